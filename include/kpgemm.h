@@ -1,0 +1,136 @@
+/*
+ * kpgemm.h -- C ABI of the B200 (sm_100a) tiled-GEMM kernel family behind the
+ * kernelprune benchmark/selection path (arXiv 2008.13145).
+ *
+ * The reference package (`kernelprune`, /root/reference/pkg) is host-only: it
+ * consumes a benchmark table and emits a selector, but the kernel, the timing
+ * harness and the launcher sit outside it. This header is the boundary those
+ * missing pieces plug into. Every entry point below names the reference
+ * interface it serves:
+ *
+ *   KernelChoice ............ the struct the emitted `select_kernel(...)` returns
+ *                             (codegen.py:185-194; the reference never defines it)
+ *                             and the 5-tuple of KernelConfig (dataset.py:39-58).
+ *   kp_gemm ................. "matmul-with-config": the kernel the paper times
+ *                             (dataset.py:41-46 tile semantics,
+ *                             dataset.py:312-316 launch geometry for family PAPER).
+ *   kp_bench ................ the benchmark harness that produces one cell of the
+ *                             CSV `m,k,n,batch,R,A,C,wgR,wgC,gflops`
+ *                             (dataset.py:36, replacing synth_generate
+ *                             dataset.py:319-347 as the PerfMatrix producer).
+ *   kp_dispatch_* ........... the runtime selector: predict_tree (classify.py:230-237)
+ *                             walked over a kptree v1 model (codegen.py:36-51) with the
+ *                             same strict '<' comparison (codegen.py:188).
+ *   kp_gemm_auto ............ select_kernel + launch in one call.
+ *
+ * Conventions
+ *   - Problem dims are passed in the reference's ProblemSize order (m, k, n, batch)
+ *     (dataset.py:61-74).  C[b] = A[b] * B[b]; A is m x k, B is k x n, C is m x n,
+ *     all row-major with leading dimensions lda/ldb/ldc (elements) and batch strides
+ *     sA/sB/sC (elements; sB == 0 broadcasts one weight matrix over the batch).
+ *   - Element types by family: PAPER/SIMT/TF32: A,B,C fp32. BF16: A,B bf16, C fp32.
+ *   - Every call returns 0 on success or a negative status (KP_E*) and records a
+ *     thread-local message readable with kp_last_error().  The Python shim maps
+ *     KP_EINVAL -> ValueError, KP_ENOENT -> KeyError/ValueError, KP_EIO -> RuntimeError
+ *     (errors.py:1-49 taxonomy).  There is no CPU fallback anywhere.
+ *   - The caller owns all device memory; no entry point allocates or frees device
+ *     buffers.  `stream` is a cudaStream_t (NULL = legacy default stream).
+ */
+#ifndef KPGEMM_H_
+#define KPGEMM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KPGEMM_ABI_VERSION 1
+
+/* Status codes (negated errno values). */
+#define KP_OK 0
+#define KP_ENOENT (-2)  /* unknown variant / no dispatch table */
+#define KP_EIO (-5)     /* CUDA launch or runtime error */
+#define KP_EINVAL (-22) /* bad config, shape, stride or alignment */
+
+/* Kernel families.  Each family has its own config list and its own benchmark
+ * table: the oracle-best denominator spans every column of a table
+ * (evaluate.py:81), so families are never mixed in one table silently. */
+#define KP_FAMILY_PAPER 0 /* F0: paper-faithful fp32 SIMT, no shared memory */
+#define KP_FAMILY_SIMT 1  /* F1: B200 fp32 SIMT, cp.async multi-stage smem pipeline, warp tiles   */
+#define KP_FAMILY_TF32 2  /* F2: tcgen05 kind::tf32, fp32 in / fp32 out                            */
+#define KP_FAMILY_BF16 3  /* F3: tcgen05 kind::f16, bf16 in / fp32 out                              */
+#define KP_NUM_FAMILIES 4
+
+/* Field order is the emitted selector's (codegen.py:191-192). */
+typedef struct KernelChoice {
+  int32_t tile_rows; /* R: output rows per work item              */
+  int32_t tile_acc;  /* A: accumulation depth per step / k vector */
+  int32_t tile_cols; /* C: output cols per work item              */
+  int32_t wg_rows;   /* work-group rows                           */
+  int32_t wg_cols;   /* work-group cols                           */
+} KernelChoice;
+
+/* ---- library / registry ------------------------------------------------ */
+int kp_abi_version(void);
+const char* kp_last_error(void);
+int kp_num_variants(void);
+/* Variant id of (family, choice), or KP_ENOENT. */
+int kp_find_variant(int family, KernelChoice choice);
+/* Registry entry of a variant id. */
+int kp_variant_info(int id, KernelChoice* choice, int* family);
+/* Number of configs of a family; their order is the family's canonical column
+ * order (enumerate_configs order, dataset.py:173-196, for PAPER and SIMT). */
+int kp_family_size(int family);
+int kp_family_variant(int family, int index);
+
+/* ---- GEMM ("matmul-with-config") --------------------------------------- */
+int kp_gemm(int id, int m, int k, int n, int batch,
+            const void* A, int64_t lda, int64_t sA,
+            const void* B, int64_t ldb, int64_t sB,
+            void* C, int64_t ldc, int64_t sC, void* stream);
+
+/* ---- benchmark harness ---------------------------------------------------
+ * warmup untimed launches, then one launch timed alone to size the loop, then
+ * max(min_iters, ceil(min_ms / t1)) (capped at max_iters) back-to-back launches
+ * bracketed by CUDA events on `stream`.  *mean_ms = elapsed / iters. */
+int kp_bench(int id, int m, int k, int n, int batch,
+             const void* A, int64_t lda, int64_t sA,
+             const void* B, int64_t ldb, int64_t sB,
+             void* C, int64_t ldc, int64_t sC,
+             int warmup, int min_iters, int max_iters, double min_ms,
+             double* mean_ms, int* iters, void* stream);
+
+/* Peak FP32 FFMA throughput probe: a register-resident FFMA loop on every SM;
+ * returns the achieved TFLOP/s in *tflops (used as the measured FP32 SIMT peak). */
+int kp_ffma_peak(double* tflops, void* stream);
+
+/* ---- runtime dispatch table (tree -> variant id) ------------------------
+ * A flattened CART tree in preorder (classify.py:56-77): internal nodes carry
+ * feature in [0,4) and threshold; leaves carry leaf_class >= 0.  class_to_variant
+ * maps the subset-local class (label_best_in_subset, classify.py:32-34) to a
+ * variant id.  Returns a table handle >= 0.  Loading is not concurrent with
+ * selection on the same handle; selection is reentrant. */
+int kp_dispatch_load(int n_nodes, const int32_t* feature, const double* threshold,
+                     const int32_t* left, const int32_t* right, const int32_t* leaf_class,
+                     int n_classes, const int32_t* class_to_variant);
+int kp_dispatch_free(int handle);
+/* Walk with features log2(m), log2(k), log2(n), log2(batch) supplied by the caller
+ * (the Python shim computes them with np.log2, classify.py:27-29).  Returns the
+ * subset-local class (>= 0) or a negative status. */
+int kp_dispatch_class_feats(int handle, const double* feats4);
+/* Same, returning the variant id. */
+int kp_dispatch_select_feats(int handle, const double* feats4);
+/* Convenience: features from the C library's log2 (exact parity caveat in DESIGN.md). */
+int kp_dispatch_select(int handle, int m, int k, int n, int batch);
+/* select + kp_gemm; *variant_out (may be NULL) receives the launched variant. */
+int kp_gemm_auto(int handle, int m, int k, int n, int batch,
+                 const void* A, int64_t lda, int64_t sA,
+                 const void* B, int64_t ldb, int64_t sB,
+                 void* C, int64_t ldc, int64_t sC, void* stream, int* variant_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KPGEMM_H_ */

@@ -1,0 +1,368 @@
+// The C ABI of libkpgemm.so (include/kpgemm.h): variant registry, GEMM launch,
+// benchmark harness, FFMA peak probe and the tree -> variant dispatch tables.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "families.h"
+#include "kpgemm.h"
+#include "tc_families.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(KP_EIO, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- registry --
+struct Variant {
+  int family;
+  KernelChoice choice;
+  int index;  // position inside the family's canonical config list
+};
+
+struct Registry {
+  std::vector<Variant> variants;
+  int family_begin[KP_NUM_FAMILIES + 1];
+  kp::GemmLaunchFn f1[kp::kPaperConfigs];
+
+  Registry() {
+    std::memset(f1, 0, sizeof(f1));
+    kp::f1_fill_wg0(f1);
+    kp::f1_fill_wg1(f1);
+    kp::f1_fill_wg2(f1);
+    kp::f1_fill_wg3(f1);
+    kp::f1_fill_wg4(f1);
+    kp::f1_fill_wg5(f1);
+    kp::f1_fill_wg6(f1);
+    kp::f1_fill_wg7(f1);
+    kp::f1_fill_wg8(f1);
+    kp::f1_fill_wg9(f1);
+    const int tiles[4] = {1, 2, 4, 8};
+    for (int fam = 0; fam < KP_NUM_FAMILIES; ++fam) {
+      family_begin[fam] = static_cast<int>(variants.size());
+      if (fam == KP_FAMILY_PAPER || fam == KP_FAMILY_SIMT) {
+        int idx = 0;
+        for (int r : tiles)
+          for (int a : tiles)
+            for (int c : tiles)
+              for (int w = 0; w < kp::kNumWgPairs; ++w) {
+                KernelChoice ch{r, a, c, kp::kWgPairs[w][0], kp::kWgPairs[w][1]};
+                variants.push_back(Variant{fam, ch, idx++});
+              }
+      } else {
+        const int count = kp::tc_family_size(fam);
+        for (int i = 0; i < count; ++i) variants.push_back(Variant{fam, kp::tc_family_choice(fam, i), i});
+      }
+    }
+    family_begin[KP_NUM_FAMILIES] = static_cast<int>(variants.size());
+  }
+};
+
+Registry& registry() {
+  static Registry r;
+  return r;
+}
+
+bool same(const KernelChoice& a, const KernelChoice& b) {
+  return a.tile_rows == b.tile_rows && a.tile_acc == b.tile_acc && a.tile_cols == b.tile_cols &&
+         a.wg_rows == b.wg_rows && a.wg_cols == b.wg_cols;
+}
+
+int check_problem(int id, int m, int k, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* B,
+                  int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC) {
+  Registry& reg = registry();
+  if (id < 0 || id >= static_cast<int>(reg.variants.size())) return fail(KP_ENOENT, "unknown variant id %d", id);
+  if (m < 1 || k < 1 || n < 1 || batch < 1)
+    return fail(KP_EINVAL, "dims must be >= 1 (m=%d k=%d n=%d batch=%d)", m, k, n, batch);
+  if (!A || !B || !C) return fail(KP_EINVAL, "null operand pointer");
+  if (lda < k || ldb < n || ldc < n) return fail(KP_EINVAL, "leading dimension smaller than the row length");
+  if (sA < 0 || sB < 0 || sC < 0) return fail(KP_EINVAL, "negative batch stride");
+  if (batch > 1 && sC < static_cast<int64_t>(m) * ldc) return fail(KP_EINVAL, "output batch stride overlaps");
+  if (batch > 65535) return fail(KP_EINVAL, "batch > 65535");
+  return KP_OK;
+}
+
+int launch(int id, const kp::GemmArgs& p, cudaStream_t s) {
+  Registry& reg = registry();
+  const Variant& v = reg.variants[id];
+  cudaError_t e = cudaSuccess;
+  switch (v.family) {
+    case KP_FAMILY_PAPER:
+      e = kp::f0_launch(v.choice, p, s);
+      break;
+    case KP_FAMILY_SIMT:
+      e = reg.f1[v.index](p, s);
+      break;
+    default: {
+      const int rc = kp::tc_check(v.family, v.index, p);
+      if (rc != KP_OK) return fail(rc, "variant %d cannot run this problem: %s", id, kp::tc_last_reason());
+      e = kp::tc_launch(v.family, v.index, p, s);
+      break;
+    }
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return KP_OK;
+}
+
+kp::GemmArgs make_args(int m, int k, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* B,
+                       int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC) {
+  kp::GemmArgs p;
+  p.m = m; p.k = k; p.n = n; p.batch = batch;
+  p.A = A; p.lda = lda; p.sA = sA;
+  p.B = B; p.ldb = ldb; p.sB = sB;
+  p.C = C; p.ldc = ldc; p.sC = sC;
+  p.a_vec = p.b_vec = p.c_vec = 0;
+  return p;
+}
+
+// ---------------------------------------------------------- dispatch tables --
+struct Table {
+  bool live = false;
+  std::vector<int32_t> feature, left, right, leaf_class, class_to_variant;
+  std::vector<double> threshold;
+};
+std::mutex g_tables_mu;
+std::vector<Table> g_tables;
+
+const Table* get_table(int handle) {
+  std::lock_guard<std::mutex> lock(g_tables_mu);
+  if (handle < 0 || handle >= static_cast<int>(g_tables.size()) || !g_tables[handle].live) return nullptr;
+  return &g_tables[handle];
+}
+
+// predict_tree (classify.py:230-237): left iff x[f] < thr, strictly.
+int walk(const Table& t, const double* x) {
+  int node = 0;
+  for (size_t steps = 0; steps <= t.feature.size(); ++steps) {
+    const int cls = t.leaf_class[node];
+    if (cls >= 0) return cls;
+    node = (x[t.feature[node]] < t.threshold[node]) ? t.left[node] : t.right[node];
+  }
+  return fail(KP_EINVAL, "tree walk did not terminate");
+}
+
+}  // namespace
+
+// ====================================================================== ABI ==
+extern "C" {
+
+int kp_abi_version(void) { return KPGEMM_ABI_VERSION; }
+
+const char* kp_last_error(void) { return g_last_error.c_str(); }
+
+int kp_num_variants(void) { return static_cast<int>(registry().variants.size()); }
+
+int kp_family_size(int family) {
+  if (family < 0 || family >= KP_NUM_FAMILIES) return fail(KP_EINVAL, "unknown family %d", family);
+  Registry& reg = registry();
+  return reg.family_begin[family + 1] - reg.family_begin[family];
+}
+
+int kp_family_variant(int family, int index) {
+  const int size = kp_family_size(family);
+  if (size < 0) return size;
+  if (index < 0 || index >= size) return fail(KP_ENOENT, "family %d has no config index %d", family, index);
+  return registry().family_begin[family] + index;
+}
+
+int kp_find_variant(int family, KernelChoice choice) {
+  if (family < 0 || family >= KP_NUM_FAMILIES) return fail(KP_EINVAL, "unknown family %d", family);
+  Registry& reg = registry();
+  for (int i = reg.family_begin[family]; i < reg.family_begin[family + 1]; ++i)
+    if (same(reg.variants[i].choice, choice)) return i;
+  return fail(KP_ENOENT, "family %d has no config (%d,%d,%d,%d,%d)", family, choice.tile_rows, choice.tile_acc,
+              choice.tile_cols, choice.wg_rows, choice.wg_cols);
+}
+
+int kp_variant_info(int id, KernelChoice* choice, int* family) {
+  Registry& reg = registry();
+  if (id < 0 || id >= static_cast<int>(reg.variants.size())) return fail(KP_ENOENT, "unknown variant id %d", id);
+  if (choice) *choice = reg.variants[id].choice;
+  if (family) *family = reg.variants[id].family;
+  return KP_OK;
+}
+
+int kp_gemm(int id, int m, int k, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* B,
+            int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, void* stream) {
+  int rc = check_problem(id, m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC);
+  if (rc != KP_OK) return rc;
+  return launch(id, make_args(m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC), static_cast<cudaStream_t>(stream));
+}
+
+int kp_bench(int id, int m, int k, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* B,
+             int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, int warmup, int min_iters, int max_iters,
+             double min_ms, double* mean_ms, int* iters, void* stream) {
+  int rc = check_problem(id, m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC);
+  if (rc != KP_OK) return rc;
+  if (!mean_ms || !iters) return fail(KP_EINVAL, "null output pointer");
+  if (min_iters < 1 || max_iters < min_iters) return fail(KP_EINVAL, "bad iteration bounds");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const kp::GemmArgs p = make_args(m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC);
+  for (int i = 0; i < warmup; ++i)
+    if ((rc = launch(id, p, s)) != KP_OK) return rc;
+  cudaEvent_t e0, e1;
+  cudaError_t e;
+  if ((e = cudaEventCreate(&e0)) != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+  if ((e = cudaEventCreate(&e1)) != cudaSuccess) {
+    cudaEventDestroy(e0);
+    return cuda_fail(e, "cudaEventCreate");
+  }
+  auto timed = [&](int count, float* ms) -> int {
+    cudaEventRecord(e0, s);
+    for (int i = 0; i < count; ++i) {
+      int r = launch(id, p, s);
+      if (r != KP_OK) return r;
+    }
+    cudaEventRecord(e1, s);
+    cudaError_t err = cudaEventSynchronize(e1);
+    if (err != cudaSuccess) return cuda_fail(err, "kernel execution");
+    err = cudaEventElapsedTime(ms, e0, e1);
+    if (err != cudaSuccess) return cuda_fail(err, "cudaEventElapsedTime");
+    return KP_OK;
+  };
+  float t1 = 0.f, tn = 0.f;
+  rc = timed(1, &t1);
+  int count = min_iters;
+  if (rc == KP_OK) {
+    const double want = t1 > 0.f ? std::ceil(min_ms / t1) : static_cast<double>(max_iters);
+    count = static_cast<int>(want < min_iters ? min_iters : (want > max_iters ? max_iters : want));
+    rc = timed(count, &tn);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc != KP_OK) return rc;
+  *mean_ms = static_cast<double>(tn) / count;
+  *iters = count;
+  return KP_OK;
+}
+
+int kp_ffma_peak(double* tflops, void* stream) {
+  if (!tflops) return fail(KP_EINVAL, "null output pointer");
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  float* sink = nullptr;
+  cudaError_t e = cudaMalloc(&sink, sizeof(float) * 1024 * 1024);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int threads = 256, blocks = sms * 8, iters = 1 << 14;
+  e = kp::ffma_peak_launch(sink, blocks, threads, 256, s);  // warm-up
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+  if (e == cudaSuccess) e = kp::ffma_peak_launch(sink, blocks, threads, iters, s);
+  cudaEventRecord(e1, s);
+  if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  if (e != cudaSuccess) return cuda_fail(e, "ffma peak probe");
+  // 16 independent FFMA chains x 8 unrolled steps per iteration, 2 flops each.
+  const double flops = 2.0 * 16.0 * 8.0 * iters * static_cast<double>(threads) * blocks;
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  return KP_OK;
+}
+
+int kp_dispatch_load(int n_nodes, const int32_t* feature, const double* threshold, const int32_t* left,
+                     const int32_t* right, const int32_t* leaf_class, int n_classes,
+                     const int32_t* class_to_variant) {
+  if (n_nodes < 1 || !feature || !threshold || !left || !right || !leaf_class)
+    return fail(KP_EINVAL, "empty tree or null array");
+  if (n_classes < 1 || !class_to_variant) return fail(KP_EINVAL, "no classes");
+  const int nv = kp_num_variants();
+  for (int c = 0; c < n_classes; ++c)
+    if (class_to_variant[c] < 0 || class_to_variant[c] >= nv)
+      return fail(KP_ENOENT, "class %d maps to unknown variant %d", c, class_to_variant[c]);
+  // Structural checks mirror import_model (codegen.py:116-145).
+  std::vector<int> seen(n_nodes, 0);
+  std::vector<int> stack{0};
+  int visited = 0;
+  while (!stack.empty()) {
+    const int v = stack.back();
+    stack.pop_back();
+    if (seen[v]) return fail(KP_EINVAL, "node %d reachable twice; not a tree", v);
+    seen[v] = 1;
+    ++visited;
+    if (leaf_class[v] >= 0) {
+      if (leaf_class[v] >= n_classes) return fail(KP_EINVAL, "leaf class %d outside %d classes", leaf_class[v], n_classes);
+      continue;
+    }
+    if (feature[v] < 0 || feature[v] >= 4) return fail(KP_EINVAL, "feature index %d out of range", feature[v]);
+    if (std::isnan(threshold[v])) return fail(KP_EINVAL, "NaN threshold at node %d", v);
+    for (int child : {left[v], right[v]}) {
+      if (child < 0 || child >= n_nodes) return fail(KP_EINVAL, "child id %d out of range", child);
+      stack.push_back(child);
+    }
+  }
+  if (visited != n_nodes) return fail(KP_EINVAL, "unreachable nodes in tree");
+  Table t;
+  t.live = true;
+  t.feature.assign(feature, feature + n_nodes);
+  t.threshold.assign(threshold, threshold + n_nodes);
+  t.left.assign(left, left + n_nodes);
+  t.right.assign(right, right + n_nodes);
+  t.leaf_class.assign(leaf_class, leaf_class + n_nodes);
+  t.class_to_variant.assign(class_to_variant, class_to_variant + n_classes);
+  std::lock_guard<std::mutex> lock(g_tables_mu);
+  g_tables.push_back(std::move(t));
+  return static_cast<int>(g_tables.size()) - 1;
+}
+
+int kp_dispatch_free(int handle) {
+  std::lock_guard<std::mutex> lock(g_tables_mu);
+  if (handle < 0 || handle >= static_cast<int>(g_tables.size()) || !g_tables[handle].live)
+    return fail(KP_ENOENT, "unknown dispatch table %d", handle);
+  g_tables[handle] = Table{};
+  return KP_OK;
+}
+
+int kp_dispatch_class_feats(int handle, const double* feats4) {
+  const Table* t = get_table(handle);
+  if (!t) return fail(KP_ENOENT, "unknown dispatch table %d", handle);
+  if (!feats4) return fail(KP_EINVAL, "null feature vector");
+  return walk(*t, feats4);
+}
+
+int kp_dispatch_select_feats(int handle, const double* feats4) {
+  const int cls = kp_dispatch_class_feats(handle, feats4);
+  if (cls < 0) return cls;
+  return get_table(handle)->class_to_variant[cls];
+}
+
+int kp_dispatch_select(int handle, int m, int k, int n, int batch) {
+  if (m < 1 || k < 1 || n < 1 || batch < 1) return fail(KP_EINVAL, "dims must be >= 1");
+  const double f[4] = {std::log2(static_cast<double>(m)), std::log2(static_cast<double>(k)),
+                       std::log2(static_cast<double>(n)), std::log2(static_cast<double>(batch))};
+  return kp_dispatch_select_feats(handle, f);
+}
+
+int kp_gemm_auto(int handle, int m, int k, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* B,
+                 int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, void* stream, int* variant_out) {
+  const int id = kp_dispatch_select(handle, m, k, n, batch);
+  if (id < 0) return id;
+  if (variant_out) *variant_out = id;
+  return kp_gemm(id, m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC, stream);
+}
+
+}  // extern "C"

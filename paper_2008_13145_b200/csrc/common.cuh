@@ -1,0 +1,95 @@
+// Shared device helpers and launch-parameter structs for the kpgemm families.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kpgemm.h"
+
+namespace kp {
+
+// Launch parameters common to every fp32 family.  Dims follow the reference's
+// ProblemSize order (m, k, n, batch), dataset.py:61-74.
+struct GemmArgs {
+  int m, k, n, batch;
+  const void* A;
+  int64_t lda, sA;
+  const void* B;
+  int64_t ldb, sB;
+  void* C;
+  int64_t ldc, sC;
+  // Host-computed alignment facts (uniform across the grid).
+  int a_vec;  // rows of A may be read with the family's vector width along k
+  int b_vec;  // rows of B may be read with the family's vector width along n
+  int c_vec;  // rows of C may be written with the family's vector width along n
+};
+
+// ---- vector load / store of N consecutive floats (N in {1,2,4,8}) ---------
+template <int N>
+__device__ __forceinline__ void ldg_vec(const float* __restrict__ p, float* out) {
+  if constexpr (N == 1) {
+    out[0] = __ldg(p);
+  } else if constexpr (N == 2) {
+    float2 v = __ldg(reinterpret_cast<const float2*>(p));
+    out[0] = v.x; out[1] = v.y;
+  } else if constexpr (N == 4) {
+    float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+  } else {
+    static_assert(N == 8, "vector width");
+    float4 v0 = __ldg(reinterpret_cast<const float4*>(p));
+    float4 v1 = __ldg(reinterpret_cast<const float4*>(p + 4));
+    out[0] = v0.x; out[1] = v0.y; out[2] = v0.z; out[3] = v0.w;
+    out[4] = v1.x; out[5] = v1.y; out[6] = v1.z; out[7] = v1.w;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void lds_vec(const float* p, float* out) {
+  if constexpr (N == 1) {
+    out[0] = p[0];
+  } else if constexpr (N == 2) {
+    float2 v = *reinterpret_cast<const float2*>(p);
+    out[0] = v.x; out[1] = v.y;
+  } else if constexpr (N == 4) {
+    float4 v = *reinterpret_cast<const float4*>(p);
+    out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+  } else {
+    static_assert(N == 8, "vector width");
+    float4 v0 = *reinterpret_cast<const float4*>(p);
+    float4 v1 = *reinterpret_cast<const float4*>(p + 4);
+    out[0] = v0.x; out[1] = v0.y; out[2] = v0.z; out[3] = v0.w;
+    out[4] = v1.x; out[5] = v1.y; out[6] = v1.z; out[7] = v1.w;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void stg_vec(float* p, const float* v) {
+  if constexpr (N == 1) {
+    p[0] = v[0];
+  } else if constexpr (N == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  } else if constexpr (N == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+    static_assert(N == 8, "vector width");
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
+// ---- cp.async (LDGSTS) with zero fill ------------------------------------
+// src_bytes == 0 writes zeros and reads nothing.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+}  // namespace kp

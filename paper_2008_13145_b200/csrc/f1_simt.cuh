@@ -1,0 +1,243 @@
+// F1 -- B200 fp32 SIMT family (KP_FAMILY_SIMT): the paper's 640-config parameter
+// space (dataset.py:41-46) re-instantiated B200-first.
+//
+// What a config means here (same 5-tuple, same per-work-item contract):
+//   * each thread (work item) owns an R x C output tile and accumulates it in
+//     registers, stepping k by A: per step it reads an R x A LHS fragment (R vector
+//     loads of width A along k) and an A x C RHS fragment (A vector loads of width
+//     min(C,4) along n) -- from shared memory instead of global memory;
+//   * the CTA is the work group: wg_rows x wg_cols threads, CTA tile
+//     BM = R*wg_rows by BN = C*wg_cols, grid = work_items() geometry
+//     (dataset.py:312-316) with the m-groups in gridDim.x.
+// B200-specific choices (not tunables; derived from the tuple at compile time):
+//   * global -> shared staging with cp.async (LDGSTS) 16-byte zero-filling copies
+//     (4-byte copies when a row is not 16-byte aligned, e.g. k = 27 or 147), in a
+//     STAGES-deep ring (2..4) sized to leave room for two CTAs per SM (<= 110 KB);
+//   * stage depth BK in {32,16,8}: the largest that fits two stages in the budget;
+//   * warp tiling: lanes form a WTR x WTC patch of the work group chosen to minimise
+//     the per-warp operand footprint WTR*R + WTC*C, so shared-memory reads are
+//     broadcast across the patch and conflict-free (padded LHS rows, RHS columns
+//     interleaved in float4 groups);
+//   * tails by zero-fill: out-of-range rows/cols/k land as zeros in shared memory and
+//     contribute fma(0, 0, acc) == acc exactly.
+// Every output element is the sequential fp32 fma chain over k = 0..K-1, so F1 is
+// bit-identical to F0 and to the oracle (oracle/gemm_ref.c).
+#pragma once
+
+#include "common.cuh"
+
+namespace kp {
+
+constexpr int f1_pick_wtc(int R, int C, int WGR, int WGC) {
+  int best = -1, best_cost = 1 << 30;
+  for (int wtc = 1; wtc <= 32; wtc *= 2) {
+    const int wtr = 32 / wtc;
+    if (WGC % wtc != 0 || WGR % wtr != 0) continue;
+    const int cost = wtr * R + wtc * C;
+    if (cost <= best_cost) {  // ties go to the wider (store-coalescing) patch
+      best_cost = cost;
+      best = wtc;
+    }
+  }
+  return best;
+}
+
+template <int R, int A, int C, int WGR, int WGC>
+struct F1Cfg {
+  static constexpr int NT = WGR * WGC;
+  static constexpr int BM = R * WGR;
+  static constexpr int BN = C * WGC;
+  static constexpr int VC = C < 4 ? C : 4;
+  static constexpr int PADA = 4;
+  static constexpr int kBudget = 110 * 1024;
+  static constexpr int stage_floats(int bk) { return BM * (bk + PADA) + bk * BN; }
+  static constexpr int BK = (2 * 4 * stage_floats(32) <= kBudget)   ? 32
+                            : (2 * 4 * stage_floats(16) <= kBudget) ? 16
+                                                                    : 8;
+  static constexpr int SA = BK + PADA;  // LHS smem row stride (floats)
+  static constexpr int SB = BN;         // RHS smem row stride (floats)
+  static constexpr int STAGE = stage_floats(BK);
+  static constexpr int STAGES_FIT = kBudget / (4 * STAGE);
+  static constexpr int STAGES = STAGES_FIT < 2 ? 2 : (STAGES_FIT > 4 ? 4 : STAGES_FIT);
+  static constexpr int SMEM_BYTES = STAGES * STAGE * 4;
+  static constexpr int WTC = f1_pick_wtc(R, C, WGR, WGC);
+  static constexpr int WTR = 32 / WTC;
+  static constexpr int WPC = WGC / WTC;  // warps across the work-group columns
+  static constexpr bool B_CHUNKS = (BN % 4) == 0;
+  static_assert(WTC > 0, "work group not tileable by warps");
+  static_assert(NT % 32 == 0, "work group must be whole warps");
+  static_assert(BK % A == 0, "stage depth must be a multiple of A");
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+};
+
+template <int R, int A, int C, int WGR, int WGC>
+__global__ void __launch_bounds__(WGR * WGC) f1_kernel(GemmArgs p, int groups_n) {
+  using Cfg = F1Cfg<R, A, C, WGR, WGC>;
+  constexpr int NT = Cfg::NT, BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
+  constexpr int SA = Cfg::SA, SB = Cfg::SB, STAGES = Cfg::STAGES, VC = Cfg::VC;
+  extern __shared__ __align__(16) float smem[];
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int ty = (warp / Cfg::WPC) * Cfg::WTR + lane / Cfg::WTC;
+  const int tx = (warp % Cfg::WPC) * Cfg::WTC + lane % Cfg::WTC;
+
+  const int64_t gm = blockIdx.x / groups_n;
+  const int gn = blockIdx.x - static_cast<int>(gm * groups_n);
+  const int b = blockIdx.y;
+  const int m = p.m, k = p.k, n = p.n;
+  const int64_t m0 = gm * BM;
+  const int64_t n0 = static_cast<int64_t>(gn) * BN;
+
+  const float* __restrict__ Ab = static_cast<const float*>(p.A) + b * p.sA;
+  const float* __restrict__ Bb = static_cast<const float*>(p.B) + b * p.sB;
+  float* __restrict__ Cb = static_cast<float*>(p.C) + b * p.sC;
+  const int64_t lda = p.lda, ldb = p.ldb;
+  const bool a16 = p.a_vec, b16 = Cfg::B_CHUNKS && p.b_vec;
+
+  auto load_tile = [&](int stage, int kt) {
+    float* as = smem + stage * Cfg::STAGE;
+    float* bs = as + BM * SA;
+    const int k0 = kt * BK;
+    if (a16) {
+      constexpr int CPR = BK / 4, CH = BM * CPR;
+#pragma unroll
+      for (int j = 0; j < (CH + NT - 1) / NT; ++j) {
+        const int c = tid + j * NT;
+        if (CH % NT == 0 || c < CH) {
+          const int r = c / CPR, q = c - r * CPR;
+          const int64_t gr = m0 + r;
+          const int gk = k0 + q * 4;
+          const bool ok = gr < m && gk < k;
+          cp_async16(as + r * SA + q * 4, ok ? Ab + gr * lda + gk : Ab, ok ? 16 : 0);
+        }
+      }
+    } else {
+      constexpr int EL = BM * BK;
+#pragma unroll 4
+      for (int j = 0; j < (EL + NT - 1) / NT; ++j) {
+        const int e = tid + j * NT;
+        if (EL % NT == 0 || e < EL) {
+          const int r = e / BK, q = e - r * BK;
+          const int64_t gr = m0 + r;
+          const int gk = k0 + q;
+          const bool ok = gr < m && gk < k;
+          cp_async4(as + r * SA + q, ok ? Ab + gr * lda + gk : Ab, ok ? 4 : 0);
+        }
+      }
+    }
+    if (b16) {
+      constexpr int CPR = BN / 4 > 0 ? BN / 4 : 1, CH = BK * CPR;
+#pragma unroll
+      for (int j = 0; j < (CH + NT - 1) / NT; ++j) {
+        const int c = tid + j * NT;
+        if (CH % NT == 0 || c < CH) {
+          const int r = c / CPR, q = c - r * CPR;
+          const int gk = k0 + r;
+          const int64_t gc = n0 + q * 4;
+          const bool ok = gk < k && gc < n;
+          cp_async16(bs + r * SB + q * 4, ok ? Bb + static_cast<int64_t>(gk) * ldb + gc : Bb, ok ? 16 : 0);
+        }
+      }
+    } else {
+      constexpr int EL = BK * BN;
+#pragma unroll 4
+      for (int j = 0; j < (EL + NT - 1) / NT; ++j) {
+        const int e = tid + j * NT;
+        if (EL % NT == 0 || e < EL) {
+          const int r = e / BN, q = e - r * BN;
+          const int gk = k0 + r;
+          const int64_t gc = n0 + q;
+          const bool ok = gk < k && gc < n;
+          cp_async4(bs + r * SB + q, ok ? Bb + static_cast<int64_t>(gk) * ldb + gc : Bb, ok ? 4 : 0);
+        }
+      }
+    }
+  };
+
+  float acc[R][C];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
+
+  const int KT = (k + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_tile(s, s);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < KT) load_tile(nk % STAGES, nk);
+      cp_async_commit();
+    }
+    const float* as = smem + (kt % STAGES) * Cfg::STAGE;
+    const float* bs = as + BM * SA;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += A) {
+      float a[R][A];
+#pragma unroll
+      for (int r = 0; r < R; ++r) lds_vec<A>(as + (r * WGR + ty) * SA + kk, a[r]);
+#pragma unroll
+      for (int i = 0; i < A; ++i) {
+        float w[C];
+#pragma unroll
+        for (int cv = 0; cv < C / VC; ++cv) lds_vec<VC>(bs + (kk + i) * SB + cv * WGC * VC + tx * VC, w + cv * VC);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int c = 0; c < C; ++c) acc[r][c] = __fmaf_rn(a[r][i], w[c], acc[r][c]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t row = m0 + r * WGR + ty;
+    if (row >= m) continue;
+    float* out = Cb + row * p.ldc;
+#pragma unroll
+    for (int cv = 0; cv < C / VC; ++cv) {
+      const int64_t col = n0 + cv * WGC * VC + tx * VC;
+      if (p.c_vec && col + VC <= n) {
+        stg_vec<VC>(out + col, &acc[r][cv * VC]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VC; ++e)
+          if (col + e < n) out[col + e] = acc[r][cv * VC + e];
+      }
+    }
+  }
+}
+
+template <int R, int A, int C, int WGR, int WGC>
+cudaError_t f1_launch(const GemmArgs& p0, cudaStream_t s) {
+  using Cfg = F1Cfg<R, A, C, WGR, WGC>;
+  static bool attr_set = false;  // benign race: idempotent attribute write
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(f1_kernel<R, A, C, WGR, WGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  GemmArgs p = p0;
+  auto aligned = [](const void* ptr, int bytes) { return (reinterpret_cast<uintptr_t>(ptr) % bytes) == 0; };
+  p.a_vec = (p.k % 4 == 0) && (p.lda % 4 == 0) && (p.sA % 4 == 0) && aligned(p.A, 16);
+  p.b_vec = (p.n % 4 == 0) && (p.ldb % 4 == 0) && (p.sB % 4 == 0) && aligned(p.B, 16);
+  p.c_vec = (p.ldc % Cfg::VC == 0) && (p.sC % Cfg::VC == 0) && aligned(p.C, 4 * Cfg::VC);
+  const int64_t groups_m = (p.m + Cfg::BM - 1) / Cfg::BM;
+  const int64_t groups_n = (p.n + Cfg::BN - 1) / Cfg::BN;
+  const int64_t gx = groups_m * groups_n;
+  if (gx > 0x7fffffffLL || p.batch > 65535) return cudaErrorInvalidConfiguration;
+  f1_kernel<R, A, C, WGR, WGC><<<dim3(static_cast<unsigned>(gx), p.batch), Cfg::NT, Cfg::SMEM_BYTES, s>>>(
+      p, static_cast<int>(groups_n));
+  return cudaGetLastError();
+}
+
+}  // namespace kp

@@ -1,0 +1,159 @@
+"""matmul-with-config: launch one variant of the sm_100a kernel family on torch
+CUDA tensors through the C ABI (include/kpgemm.h, ``kp_gemm``).
+
+The reference describes the kernel only as a contract -- a config is
+``KernelConfig(R, A, C, wg_rows, wg_cols)`` (dataset.py:39-58) and the kernel
+computes C = A @ B per batch.  This module is that operator.
+Families (include/kpgemm.h): ``paper`` (F0, paper-faithful, no shared memory),
+``simt`` (F1, B200 SIMT pipeline), ``tf32`` / ``bf16`` (tcgen05 tensor cores).
+There is no CPU or library fallback: a missing kernel library raises.
+"""
+
+from __future__ import annotations
+
+from functools import lru_cache
+
+import torch
+
+from . import _lib
+from .dataset import KernelConfig, ProblemSize
+
+FAMILIES = ("paper", "simt", "tf32", "bf16")
+
+
+def _family_id(family: str | int) -> int:
+    if isinstance(family, int):
+        if family not in _lib.FAMILY_NAMES:
+            raise ValueError(f"unknown family {family!r}")
+        return family
+    try:
+        return _lib.FAMILY_IDS[family]
+    except KeyError:
+        raise ValueError(f"unknown family {family!r}, expected one of {FAMILIES}") from None
+
+
+@lru_cache(maxsize=None)
+def variant_id(config: KernelConfig, family: str | int = "simt") -> int:
+    """Kernel-library variant id of (family, config); KeyError if absent."""
+    lib = _lib.load()
+    choice = _lib.KernelChoice(*config.as_tuple())
+    return _lib.check(lib.kp_find_variant(_family_id(family), choice),
+                      f"kp_find_variant({family}, {config.as_tuple()})")
+
+
+def variant_info(vid: int) -> tuple[KernelConfig, str]:
+    lib = _lib.load()
+    choice = _lib.KernelChoice()
+    fam = _lib.ctypes.c_int()
+    _lib.check(lib.kp_variant_info(vid, _lib.ctypes.byref(choice), _lib.ctypes.byref(fam)),
+               f"kp_variant_info({vid})")
+    return KernelConfig(*choice.as_tuple()), _lib.FAMILY_NAMES[fam.value]
+
+
+@lru_cache(maxsize=None)
+def family_configs(family: str | int) -> tuple[KernelConfig, ...]:
+    """The family's canonical config list (its benchmark-table column order)."""
+    lib = _lib.load()
+    fid = _family_id(family)
+    size = _lib.check(lib.kp_family_size(fid), "kp_family_size")
+    return tuple(variant_info(_lib.check(lib.kp_family_variant(fid, i), "kp_family_variant"))[0]
+                 for i in range(size))
+
+
+def input_dtype(family: str | int) -> torch.dtype:
+    return torch.bfloat16 if _family_id(family) == _lib.FAMILY_BF16 else torch.float32
+
+
+class GemmOperands:
+    """Validated (batch, m, k) x (batch, k, n) operand view for the C ABI."""
+
+    __slots__ = ("A", "B", "C", "m", "k", "n", "batch", "lda", "sA", "ldb", "sB", "ldc", "sC")
+
+    def __init__(self, A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None, dtype: torch.dtype):
+        if A.dim() not in (2, 3) or B.dim() not in (2, 3):
+            raise ValueError("A and B must be 2-D (m,k)/(k,n) or 3-D batched")
+        if not (A.is_cuda and B.is_cuda):
+            raise ValueError("operands must be CUDA tensors (there is no CPU path)")
+        if A.dtype != dtype or B.dtype != dtype:
+            raise ValueError(f"operands must be {dtype}, got {A.dtype} and {B.dtype}")
+        A3 = A if A.dim() == 3 else A.unsqueeze(0)
+        B3 = B if B.dim() == 3 else B.unsqueeze(0)
+        batch = max(A3.shape[0], B3.shape[0])
+        for name, t in (("A", A3), ("B", B3)):
+            if t.shape[0] not in (1, batch):
+                raise ValueError(f"{name} batch {t.shape[0]} does not broadcast to {batch}")
+            if t.stride(2) != 1:
+                raise ValueError(f"{name} rows must be contiguous (stride(-1) == 1)")
+        m, k = A3.shape[1], A3.shape[2]
+        if B3.shape[1] != k:
+            raise ValueError(f"inner dimensions differ: A is (.., {m}, {k}), B is (.., {B3.shape[1]}, {B3.shape[2]})")
+        n = B3.shape[2]
+        if out is None:
+            out = torch.empty((batch, m, n), device=A.device, dtype=torch.float32)
+        elif out.dtype != torch.float32 or tuple(out.shape[-2:]) != (m, n) or out.stride(-1) != 1:
+            raise ValueError("out must be float32 (.., m, n) with contiguous rows")
+        C3 = out if out.dim() == 3 else out.unsqueeze(0)
+        self.A, self.B, self.C = A3, B3, C3
+        self.m, self.k, self.n, self.batch = m, k, n, batch
+        self.lda = A3.stride(1) if m > 1 else k
+        self.ldb = B3.stride(1) if k > 1 else n
+        self.ldc = C3.stride(1) if m > 1 else n
+        self.sA = A3.stride(0) if A3.shape[0] > 1 else 0
+        self.sB = B3.stride(0) if B3.shape[0] > 1 else 0
+        self.sC = C3.stride(0) if batch > 1 else m * self.ldc
+
+    def args(self):
+        return (self.m, self.k, self.n, self.batch,
+                self.A.data_ptr(), self.lda, self.sA,
+                self.B.data_ptr(), self.ldb, self.sB,
+                self.C.data_ptr(), self.ldc, self.sC)
+
+    @property
+    def problem(self) -> ProblemSize:
+        return ProblemSize(self.m, self.k, self.n, self.batch)
+
+
+def _squeeze_like(C3: torch.Tensor, A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
+    return C3 if (A.dim() == 3 or B.dim() == 3) else C3[0]
+
+
+def launch(vid: int, ops: GemmOperands, stream: torch.cuda.Stream | None = None) -> None:
+    lib = _lib.load()
+    s = (stream or torch.cuda.current_stream(ops.A.device)).cuda_stream
+    _lib.check(lib.kp_gemm(vid, *ops.args(), s), f"kp_gemm(variant {vid}, {ops.problem})")
+
+
+def matmul(A: torch.Tensor, B: torch.Tensor, config: KernelConfig, family: str = "simt",
+           out: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """C = A @ B with the kernel variant ``(family, config)``.
+
+    A: (m, k) or (batch, m, k); B: (k, n) or (batch, k, n) -- a 2-D operand is
+    broadcast over the batch (stride 0, e.g. conv weights).  fp32 operands for
+    paper/simt/tf32, bf16 for bf16; the result is fp32.
+    """
+    vid = variant_id(config, family)
+    ops = GemmOperands(A, B, out, input_dtype(family))
+    launch(vid, ops, stream)
+    return _squeeze_like(ops.C, A, B)
+
+
+def bench(vid: int, ops: GemmOperands, warmup: int = 1, min_iters: int = 2, max_iters: int = 10000,
+          min_ms: float = 2.0, stream: torch.cuda.Stream | None = None) -> tuple[float, int]:
+    """Mean milliseconds per launch by CUDA events (``kp_bench``) and the loop count."""
+    lib = _lib.load()
+    s = (stream or torch.cuda.current_stream(ops.A.device)).cuda_stream
+    mean = _lib.ctypes.c_double()
+    iters = _lib.ctypes.c_int()
+    _lib.check(lib.kp_bench(vid, *ops.args(), warmup, min_iters, max_iters, float(min_ms),
+                            _lib.ctypes.byref(mean), _lib.ctypes.byref(iters), s),
+               f"kp_bench(variant {vid}, {ops.problem})")
+    return mean.value, iters.value
+
+
+def ffma_peak_tflops(stream: torch.cuda.Stream | None = None) -> float:
+    """Measured FP32 FFMA peak of the current device (kp_ffma_peak)."""
+    lib = _lib.load()
+    s = (stream or torch.cuda.current_stream()).cuda_stream
+    out = _lib.ctypes.c_double()
+    _lib.check(lib.kp_ffma_peak(_lib.ctypes.byref(out), s), "kp_ffma_peak")
+    return out.value
