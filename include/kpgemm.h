@@ -101,9 +101,10 @@ int kp_bench(int id, int m, int k, int n, int batch,
              int warmup, int min_iters, int max_iters, double min_ms,
              double* mean_ms, int* iters, void* stream);
 
-/* Peak FP32 FFMA throughput probe: a register-resident FFMA loop on every SM;
- * returns the achieved TFLOP/s in *tflops (used as the measured FP32 SIMT peak). */
-int kp_ffma_peak(double* tflops, void* stream);
+/* Peak FP32 throughput probe: register-resident FMA chains on every SM, scalar
+ * FFMA (packed = 0) or sm_100 packed FFMA2 (packed = 1); returns TFLOP/s in *tflops
+ * (the measured FP32 SIMT peak the SIMT families' roofline fraction uses). */
+int kp_ffma_peak(int packed, double* tflops, void* stream);
 
 /* ---- runtime dispatch table (tree -> variant id) ------------------------
  * A flattened CART tree in preorder (classify.py:56-77): internal nodes carry

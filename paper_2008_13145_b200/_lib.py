@@ -67,7 +67,7 @@ SIGNATURES = {
     "kp_family_variant": (_i, [_i, _i]),
     "kp_gemm": (_i, [_i] + _GEMM_ARGS + [_vp]),
     "kp_bench": (_i, [_i] + _GEMM_ARGS + [_i, _i, _i, ctypes.c_double, _dp, _ip, _vp]),
-    "kp_ffma_peak": (_i, [_dp, _vp]),
+    "kp_ffma_peak": (_i, [_i, _dp, _vp]),
     "kp_dispatch_load": (_i, [_i, _i32p, _dp, _i32p, _i32p, _i32p, _i, _i32p]),
     "kp_dispatch_free": (_i, [_i]),
     "kp_dispatch_class_feats": (_i, [_i, _dp]),

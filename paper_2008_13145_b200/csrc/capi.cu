@@ -254,7 +254,7 @@ int kp_bench(int id, int m, int k, int n, int batch, const void* A, int64_t lda,
   return KP_OK;
 }
 
-int kp_ffma_peak(double* tflops, void* stream) {
+int kp_ffma_peak(int packed, double* tflops, void* stream) {
   if (!tflops) return fail(KP_EINVAL, "null output pointer");
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -264,12 +264,12 @@ int kp_ffma_peak(double* tflops, void* stream) {
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int threads = 256, blocks = sms * 8, iters = 1 << 14;
-  e = kp::ffma_peak_launch(sink, blocks, threads, 256, s);  // warm-up
+  e = kp::ffma_peak_launch(sink, blocks, threads, 256, packed != 0, s);  // warm-up
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, s);
-  if (e == cudaSuccess) e = kp::ffma_peak_launch(sink, blocks, threads, iters, s);
+  if (e == cudaSuccess) e = kp::ffma_peak_launch(sink, blocks, threads, iters, packed != 0, s);
   cudaEventRecord(e1, s);
   if (e == cudaSuccess) e = cudaEventSynchronize(e1);
   float ms = 0.f;

@@ -12,7 +12,7 @@
 // B200-specific choices (not tunables; derived from the tuple at compile time):
 //   * global -> shared staging with cp.async (LDGSTS) 16-byte zero-filling copies
 //     (4-byte copies when a row is not 16-byte aligned, e.g. k = 27 or 147), in a
-//     STAGES-deep ring (2..4) sized to leave room for two CTAs per SM (<= 110 KB);
+//     STAGES-deep ring (2..4) sized so the occupancy target below fits in 227 KB;
 //   * stage depth BK in {32,16,8}: the largest that fits two stages in the budget;
 //   * warp tiling: lanes form a WTR x WTC patch of the work group chosen to minimise
 //     the per-warp operand footprint WTR*R + WTC*C, so shared-memory reads are
@@ -49,7 +49,11 @@ struct F1Cfg {
   static constexpr int BN = C * WGC;
   static constexpr int VC = C < 4 ? C : 4;
   static constexpr int PADA = 4;
-  static constexpr int kBudget = 110 * 1024;
+  // Occupancy target: >= 16 resident warps per SM (4 per scheduler) so FFMA2 issue
+  // hides LDS latency.  MIN_BLOCKS feeds __launch_bounds__ (caps registers at
+  // 65536 / (MIN_BLOCKS * NT)) and the per-CTA shared-memory budget.
+  static constexpr int MIN_BLOCKS = (512 / NT) > 1 ? (512 / NT) : 1;
+  static constexpr int kBudget = (227 * 1024) / (MIN_BLOCKS < 4 ? MIN_BLOCKS : 4) - 1024;
   static constexpr int stage_floats(int bk) { return BM * (bk + PADA) + bk * BN; }
   static constexpr int BK = (2 * 4 * stage_floats(32) <= kBudget)   ? 32
                             : (2 * 4 * stage_floats(16) <= kBudget) ? 16
@@ -71,7 +75,7 @@ struct F1Cfg {
 };
 
 template <int R, int A, int C, int WGR, int WGC>
-__global__ void __launch_bounds__(WGR * WGC) f1_kernel(GemmArgs p, int groups_n) {
+__global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCKS) f1_kernel(GemmArgs p, int groups_n) {
   using Cfg = F1Cfg<R, A, C, WGR, WGC>;
   constexpr int NT = Cfg::NT, BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
   constexpr int SA = Cfg::SA, SB = Cfg::SB, STAGES = Cfg::STAGES, VC = Cfg::VC;
@@ -155,11 +159,15 @@ __global__ void __launch_bounds__(WGR * WGC) f1_kernel(GemmArgs p, int groups_n)
     }
   };
 
-  float acc[R][C];
+  // Accumulators as column pairs: the outer product a[r] * w[c:c+2] maps onto one
+  // FFMA2 (sm_100 packed fp32 FMA, scalar-broadcast first operand) -- half the issue
+  // slots of scalar FFMA and the same per-lane IEEE fma, so results stay bit-exact.
+  constexpr int CP = (C + 1) / 2;
+  float2 acc[R][CP];
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int c = 0; c < C; ++c) acc[r][c] = 0.0f;
+    for (int c = 0; c < CP; ++c) acc[r][c] = make_float2(0.0f, 0.0f);
 
   const int KT = (k + BK - 1) / BK;
 #pragma unroll
@@ -188,10 +196,16 @@ __global__ void __launch_bounds__(WGR * WGC) f1_kernel(GemmArgs p, int groups_n)
         float w[C];
 #pragma unroll
         for (int cv = 0; cv < C / VC; ++cv) lds_vec<VC>(bs + (kk + i) * SB + cv * WGC * VC + tx * VC, w + cv * VC);
+        if constexpr (C == 1) {
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+          for (int r = 0; r < R; ++r) acc[r][0].x = __fmaf_rn(a[r][i], w[0], acc[r][0].x);
+        } else {
 #pragma unroll
-          for (int c = 0; c < C; ++c) acc[r][c] = __fmaf_rn(a[r][i], w[c], acc[r][c]);
+          for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < CP; ++c)
+              acc[r][c] = __ffma2_rn(make_float2(a[r][i], a[r][i]), make_float2(w[2 * c], w[2 * c + 1]), acc[r][c]);
+        }
       }
     }
   }
@@ -205,12 +219,18 @@ __global__ void __launch_bounds__(WGR * WGC) f1_kernel(GemmArgs p, int groups_n)
 #pragma unroll
     for (int cv = 0; cv < C / VC; ++cv) {
       const int64_t col = n0 + cv * WGC * VC + tx * VC;
+      float v[VC];
+#pragma unroll
+      for (int e = 0; e < VC; ++e) {
+        const float2 pr = acc[r][(cv * VC + e) / 2];
+        v[e] = ((cv * VC + e) & 1) ? pr.y : pr.x;
+      }
       if (p.c_vec && col + VC <= n) {
-        stg_vec<VC>(out + col, &acc[r][cv * VC]);
+        stg_vec<VC>(out + col, v);
       } else {
 #pragma unroll
         for (int e = 0; e < VC; ++e)
-          if (col + e < n) out[col + e] = acc[r][cv * VC + e];
+          if (col + e < n) out[col + e] = v[e];
       }
     }
   }

@@ -34,6 +34,6 @@ void f1_fill_wg8(GemmLaunchFn* table);
 void f1_fill_wg9(GemmLaunchFn* table);
 
 // FFMA peak probe.
-cudaError_t ffma_peak_launch(float* sink, int blocks, int threads, int iters, cudaStream_t s);
+cudaError_t ffma_peak_launch(float* sink, int blocks, int threads, int iters, bool packed, cudaStream_t s);
 
 }  // namespace kp

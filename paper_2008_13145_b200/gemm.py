@@ -150,10 +150,11 @@ def bench(vid: int, ops: GemmOperands, warmup: int = 1, min_iters: int = 2, max_
     return mean.value, iters.value
 
 
-def ffma_peak_tflops(stream: torch.cuda.Stream | None = None) -> float:
-    """Measured FP32 FFMA peak of the current device (kp_ffma_peak)."""
+def ffma_peak_tflops(packed: bool = False, stream: torch.cuda.Stream | None = None) -> float:
+    """Measured FP32 peak of the current device (kp_ffma_peak): scalar FFMA or,
+    with ``packed``, sm_100 FFMA2."""
     lib = _lib.load()
     s = (stream or torch.cuda.current_stream()).cuda_stream
     out = _lib.ctypes.c_double()
-    _lib.check(lib.kp_ffma_peak(_lib.ctypes.byref(out), s), "kp_ffma_peak")
+    _lib.check(lib.kp_ffma_peak(int(packed), _lib.ctypes.byref(out), s), "kp_ffma_peak")
     return out.value
