@@ -93,7 +93,9 @@ int kp_gemm(int id, int m, int k, int n, int batch,
 /* ---- benchmark harness ---------------------------------------------------
  * warmup untimed launches, then one launch timed alone to size the loop, then
  * max(min_iters, ceil(min_ms / t1)) (capped at max_iters) back-to-back launches
- * bracketed by CUDA events on `stream`.  *mean_ms = elapsed / iters. */
+ * bracketed by CUDA events on `stream`.  *mean_ms = elapsed / iters.  When
+ * min_iters <= 1 and the single launch already took >= min_ms it is the measurement
+ * (*iters = 1). */
 int kp_bench(int id, int m, int k, int n, int batch,
              const void* A, int64_t lda, int64_t sA,
              const void* B, int64_t ldb, int64_t sB,

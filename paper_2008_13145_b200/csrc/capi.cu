@@ -242,9 +242,14 @@ int kp_bench(int id, int m, int k, int n, int batch, const void* A, int64_t lda,
   rc = timed(1, &t1);
   int count = min_iters;
   if (rc == KP_OK) {
-    const double want = t1 > 0.f ? std::ceil(min_ms / t1) : static_cast<double>(max_iters);
-    count = static_cast<int>(want < min_iters ? min_iters : (want > max_iters ? max_iters : want));
-    rc = timed(count, &tn);
+    if (min_iters <= 1 && t1 >= min_ms) {
+      tn = t1;  // a launch that alone fills the time budget is its own measurement
+      count = 1;
+    } else {
+      const double want = t1 > 0.f ? std::ceil(min_ms / t1) : static_cast<double>(max_iters);
+      count = static_cast<int>(want < min_iters ? min_iters : (want > max_iters ? max_iters : want));
+      rc = timed(count, &tn);
+    }
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

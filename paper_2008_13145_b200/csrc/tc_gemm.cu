@@ -1,10 +1,381 @@
-// Placeholder until the tcgen05 families land: both tensor-core families are empty.
+// F2 (TF32) and F3 (BF16) -- tcgen05 tensor-core families (KP_FAMILY_TF32/BF16).
+//
+// Extra candidates beside the paper's SIMT space (BASELINE.json north_star): same
+// operator contract as kp_gemm (C[b] = A[b] * B[b], row-major, fp32 out), computed
+// on the 5th-generation tensor cores:
+//   * TMA (cp.async.bulk.tensor) loads 128-byte-swizzled tiles into a STAGES-deep
+//     shared-memory ring, signalling full/empty mbarriers;
+//   * one elected thread issues tcgen05.mma (M=128, N=BN, K=32 bytes per instruction)
+//     with A K-major and B MN-major (B is row-major K x N, so no transpose pass),
+//     accumulating in TMEM (BN fp32 columns x 128 lanes);
+//   * tcgen05.commit frees each smem stage and finally signals the epilogue warps,
+//     which drain TMEM with tcgen05.ld (32x32b) and store fp32 rows.
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA
+// issuer, warps 2..5 = epilogue (warp % 4 selects the TMEM lane quadrant).
+//
+// Config 5-tuple of these families (include/kpgemm.h KernelChoice), documented in
+// (tile_rows, tile_acc, tile_cols, wg_rows, wg_cols) =
+//   (BM = 128, BK = elements per 128-byte K slab, BN, STAGES, threads = 192).
+//
+// Numerics: BF16 operands are exact bf16 inputs, fp32 accumulation.  TF32 reads fp32
+// operands and uses their top 19 bits (truncation), fp32 accumulation; tolerances in
+// tests/test_tc_gpu.py: |C - C64| <= (2*eps_in + 2*k*2^-24) * (|A||B|)_ij.
+#include <cuda.h>
+
+#include <cstdio>
+#include <cstring>
+
 #include "tc_families.h"
 
 namespace kp {
-int tc_family_size(int) { return 0; }
-KernelChoice tc_family_choice(int, int) { return KernelChoice{0, 0, 0, 0, 0}; }
-int tc_check(int, int, const GemmArgs&) { return KP_EINVAL; }
-const char* tc_last_reason() { return "tensor-core families not built"; }
-cudaError_t tc_launch(int, int, const GemmArgs&, cudaStream_t) { return cudaErrorInvalidValue; }
+namespace {
+
+constexpr int kThreads = 192;
+constexpr int BM = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "KP_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra KP_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Shared-memory matrix descriptor, SWIZZLE_128B, version 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // version
+  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+
+template <bool kTF32>
+__device__ __forceinline__ void mma_issue(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accum) {
+  if constexpr (kTF32) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  } else {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  }
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <bool kTF32, int BN, int STAGES>
+struct TcCfg {
+  static constexpr int ES = kTF32 ? 4 : 2;          // operand element size
+  static constexpr int BK = 128 / ES;               // elements per 128-byte K slab
+  static constexpr int UK = 32 / ES;                // K per tcgen05.mma (32 bytes)
+  static constexpr int NATOM = 128 / ES;            // N elements per 128-byte swizzle atom
+  static constexpr int A_BYTES = BM * 128;          // one stage of A (K-major)
+  static constexpr int B_BYTES = BK * BN * ES;      // one stage of B (MN-major atoms)
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t IDESC = (1u << 4)                      // D = f32
+                                    | ((kTF32 ? 2u : 1u) << 7)     // A = tf32 / bf16
+                                    | ((kTF32 ? 2u : 1u) << 10)    // B = tf32 / bf16
+                                    | (0u << 15)                   // A K-major
+                                    | (1u << 16)                   // B MN-major
+                                    | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
+  static_assert(BN % NATOM == 0 && BN >= 16 && BN <= 256, "tile N");
+  static_assert(SMEM_BYTES <= 227 * 1024, "smem");
+};
+
+template <bool kTF32, int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, GemmArgs p,
+                   int tiles_m, int a_batched, int b_batched) {
+  using Cfg = TcCfg<kTF32, BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile_m = blockIdx.x % tiles_m, tile_n = blockIdx.x / tiles_m;
+  const int b = blockIdx.y;
+  const int m0 = tile_m * BM, n0 = tile_n * BN;
+  const int KT = (p.k + Cfg::BK - 1) / Cfg::BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    const int za = a_batched ? b : 0, zb = b_batched ? b : 0;
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % STAGES;
+      if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+      uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
+      uint8_t* sb = sa + Cfg::A_BYTES;
+      mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
+      tma_load_3d(sa, &mapA, &full[s], kt * Cfg::BK, m0, za);
+#pragma unroll
+      for (int j = 0; j < BN / Cfg::NATOM; ++j)
+        tma_load_3d(sb + j * (Cfg::BK * 128), &mapB, &full[s], n0 + j * Cfg::NATOM, kt * Cfg::BK, zb);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % STAGES;
+      mbar_wait(&full[s], (kt / STAGES) & 1);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
+      const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < Cfg::BK / Cfg::UK; ++kk) {
+        const uint64_t adesc = smem_desc(sa + kk * 32, 16, 1024);
+        const uint64_t bdesc = smem_desc(sb + kk * Cfg::UK * 128, Cfg::BK * 128, 1024);
+        mma_issue<kTF32>(tmem_base, adesc, bdesc, Cfg::IDESC, (kt | kk) != 0);
+      }
+      mma_commit(&empty[s]);
+    }
+    mma_commit(tmem_full);
+  } else if (warp >= 2) {
+    // ---------------- epilogue: TMEM -> registers -> global ----------------
+    const int quad = warp & 3;
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int row = m0 + quad * 32 + lane;
+    float* out = static_cast<float*>(p.C) + static_cast<int64_t>(b) * p.sC + static_cast<int64_t>(row) * p.ldc;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      float v[16];
+      tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + c, v);
+      if (row < p.m) {
+        const int col = n0 + c;
+        if (p.c_vec && col + 16 <= p.n) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<float4*>(out + col + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (col + e < p.n) out[col + e] = v[e];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------- host side --
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(ptr);
+  }
+  return fn;
+}
+
+thread_local char g_reason[256] = "";
+
+struct TcConfig {
+  bool tf32;
+  int bn, stages;
+};
+
+// The family config lists (index order = the family's canonical column order).
+constexpr TcConfig kTf32Configs[] = {{true, 32, 4},  {true, 64, 4},  {true, 128, 4}, {true, 256, 4},
+                                     {true, 64, 8},  {true, 128, 6}, {true, 256, 3}, {true, 192, 4}};
+constexpr TcConfig kBf16Configs[] = {{false, 64, 4},  {false, 128, 4}, {false, 256, 4}, {false, 64, 8},
+                                     {false, 128, 6}, {false, 256, 3}, {false, 128, 2}, {false, 192, 4}};
+constexpr int kNumTc = 8;
+
+const TcConfig* config_of(int family, int index) {
+  if (index < 0 || index >= kNumTc) return nullptr;
+  if (family == KP_FAMILY_TF32) return &kTf32Configs[index];
+  if (family == KP_FAMILY_BF16) return &kBf16Configs[index];
+  return nullptr;
+}
+
+template <bool kTF32, int BN, int STAGES>
+cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
+  using Cfg = TcCfg<kTF32, BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<kTF32, BN, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  EncodeFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  GemmArgs p = p0;
+  const CUtensorMapDataType dt = kTF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const int a_batched = (p.batch > 1 && p.sA != 0), b_batched = (p.batch > 1 && p.sB != 0);
+  CUtensorMap ma, mb;
+  {
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.k), static_cast<cuuint64_t>(p.m),
+                          static_cast<cuuint64_t>(a_batched ? p.batch : 1)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.lda) * Cfg::ES,
+                             static_cast<cuuint64_t>(a_batched ? p.sA : p.lda * p.m) * Cfg::ES};
+    if (!a_batched) strides[1] = (strides[1] + 15) / 16 * 16;
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(Cfg::BK), static_cast<cuuint32_t>(BM), 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&ma, dt, 3, const_cast<void*>(p.A), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.n), static_cast<cuuint64_t>(p.k),
+                          static_cast<cuuint64_t>(b_batched ? p.batch : 1)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.ldb) * Cfg::ES,
+                             static_cast<cuuint64_t>(b_batched ? p.sB : p.ldb * p.k) * Cfg::ES};
+    if (!b_batched) strides[1] = (strides[1] + 15) / 16 * 16;
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(Cfg::NATOM), static_cast<cuuint32_t>(Cfg::BK), 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&mb, dt, 3, const_cast<void*>(p.B), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  auto aligned = [](const void* ptr, int bytes) { return (reinterpret_cast<uintptr_t>(ptr) % bytes) == 0; };
+  p.c_vec = (p.ldc % 4 == 0) && (p.sC % 4 == 0) && aligned(p.C, 16);
+  const int tiles_m = (p.m + BM - 1) / BM, tiles_n = (p.n + BN - 1) / BN;
+  dim3 grid(tiles_m * tiles_n, p.batch);
+  tc_gemm_kernel<kTF32, BN, STAGES><<<grid, kThreads, Cfg::SMEM_BYTES, s>>>(ma, mb, p, tiles_m, a_batched, b_batched);
+  return cudaGetLastError();
+}
+
+template <bool kTF32>
+cudaError_t dispatch(const TcConfig& c, const GemmArgs& p, cudaStream_t s) {
+  switch (c.bn * 16 + c.stages) {
+    case 32 * 16 + 4:
+      if constexpr (kTF32) return launch_tc<kTF32, 32, 4>(p, s);
+      return cudaErrorInvalidValue;
+    case 64 * 16 + 4: return launch_tc<kTF32, 64, 4>(p, s);
+    case 128 * 16 + 4: return launch_tc<kTF32, 128, 4>(p, s);
+    case 256 * 16 + 4: return launch_tc<kTF32, 256, 4>(p, s);
+    case 64 * 16 + 8: return launch_tc<kTF32, 64, 8>(p, s);
+    case 128 * 16 + 6: return launch_tc<kTF32, 128, 6>(p, s);
+    case 256 * 16 + 3: return launch_tc<kTF32, 256, 3>(p, s);
+    case 128 * 16 + 2:
+      if constexpr (!kTF32) return launch_tc<kTF32, 128, 2>(p, s);
+      return cudaErrorInvalidValue;
+    case 192 * 16 + 4: return launch_tc<kTF32, 192, 4>(p, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace
+
+int tc_family_size(int family) { return (family == KP_FAMILY_TF32 || family == KP_FAMILY_BF16) ? kNumTc : 0; }
+
+KernelChoice tc_family_choice(int family, int index) {
+  const TcConfig* c = config_of(family, index);
+  if (!c) return KernelChoice{0, 0, 0, 0, 0};
+  return KernelChoice{BM, c->tf32 ? 32 : 64, c->bn, c->stages, kThreads};
+}
+
+const char* tc_last_reason() { return g_reason; }
+
+int tc_check(int family, int index, const GemmArgs& p) {
+  const TcConfig* c = config_of(family, index);
+  if (!c) {
+    snprintf(g_reason, sizeof(g_reason), "no tensor-core config %d in family %d", index, family);
+    return KP_ENOENT;
+  }
+  const int es = c->tf32 ? 4 : 2;
+  auto aligned = [](const void* ptr, int bytes) { return (reinterpret_cast<uintptr_t>(ptr) % bytes) == 0; };
+  // TMA: 16-byte aligned base addresses and row / batch strides.
+  if (!aligned(p.A, 16) || !aligned(p.B, 16) || (p.lda * es) % 16 || (p.ldb * es) % 16 ||
+      (p.batch > 1 && ((p.sA * es) % 16 || (p.sB * es) % 16))) {
+    snprintf(g_reason, sizeof(g_reason),
+             "TMA needs 16-byte aligned operands and row strides (lda=%lld ldb=%lld, %d-byte elements)",
+             static_cast<long long>(p.lda), static_cast<long long>(p.ldb), es);
+    return KP_EINVAL;
+  }
+  return KP_OK;
+}
+
+cudaError_t tc_launch(int family, int index, const GemmArgs& p, cudaStream_t s) {
+  const TcConfig* c = config_of(family, index);
+  if (!c) return cudaErrorInvalidValue;
+  return c->tf32 ? dispatch<true>(*c, p, s) : dispatch<false>(*c, p, s);
+}
+
 }  // namespace kp

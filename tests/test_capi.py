@@ -1,0 +1,120 @@
+"""The C ABI without a GPU: libkpgemm.so loads, exports every symbol include/kpgemm.h
+declares, and its host-only entry points (registry, dispatch tables, error codes)
+behave.  The dispatch table must route exactly like predict_tree (classify.py:230-237)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_2008_13145_b200 import _lib
+from paper_2008_13145_b200.classify import TREE_PRESETS, predict_tree, predict_tree_batch, train_tree
+from paper_2008_13145_b200.dataset import DEFAULT_WG_PAIRS, KernelConfig, ProblemSize, enumerate_configs
+from paper_2008_13145_b200.selection import ConfigSubset
+
+HEADER = (ROOT / "include" / "kpgemm.h").read_text()
+
+
+def declared_symbols():
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(kp_\w+)\s*\(", HEADER, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    return _lib.load()
+
+
+def test_every_declared_symbol_is_exported(lib):
+    syms = declared_symbols()
+    assert len(syms) >= 16
+    for name in syms:
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, f"{name} missing from the ctypes binding"
+
+
+def test_registry_order_is_enumerate_configs(lib):
+    assert lib.kp_abi_version() == 1
+    for fam in (_lib.FAMILY_PAPER, _lib.FAMILY_SIMT):
+        assert lib.kp_family_size(fam) == 640
+        for idx, cfg in enumerate(enumerate_configs()):
+            vid = lib.kp_family_variant(fam, idx)
+            assert lib.kp_find_variant(fam, _lib.KernelChoice(*cfg.as_tuple())) == vid
+            ch = _lib.KernelChoice()
+            f = ctypes.c_int()
+            assert lib.kp_variant_info(vid, ctypes.byref(ch), ctypes.byref(f)) == 0
+            assert ch.as_tuple() == cfg.as_tuple() and f.value == fam
+
+
+def test_error_codes_and_messages(lib):
+    assert lib.kp_find_variant(_lib.FAMILY_SIMT, _lib.KernelChoice(3, 1, 1, 8, 8)) == _lib.KP_ENOENT
+    assert b"no config" in lib.kp_last_error()
+    assert lib.kp_family_size(99) == _lib.KP_EINVAL
+    with pytest.raises(KeyError):
+        _lib.check(lib.kp_variant_info(10 ** 6, None, None), "x")
+    # shape validation happens before any CUDA call
+    assert lib.kp_gemm(0, 0, 4, 4, 1, 8, 4, 0, 8, 4, 0, 8, 4, 0, None) == _lib.KP_EINVAL
+    assert lib.kp_gemm(0, 4, 4, 4, 1, None, 4, 0, 8, 4, 0, 8, 4, 0, None) == _lib.KP_EINVAL
+    assert lib.kp_gemm(0, 4, 8, 4, 1, 8, 4, 0, 8, 4, 0, 8, 4, 0, None) == _lib.KP_EINVAL  # lda < k
+    with pytest.raises(ValueError):
+        _lib.check(_lib.KP_EINVAL, "x")
+    with pytest.raises(RuntimeError):
+        _lib.check(_lib.KP_EIO, "x")
+
+
+def _random_tree(seed, n_classes=5, rows=300):
+    rng = np.random.default_rng(seed)
+    feats = np.log2(rng.integers(1, 1 << 14, size=(rows, 4)).astype(np.float64))
+    labels = rng.integers(0, n_classes, size=rows)
+    return train_tree(feats, labels, TREE_PRESETS["A"], n_classes=n_classes)
+
+
+def _load(lib, tree, variants):
+    arrs = [np.ascontiguousarray(a, dtype=t) for a, t in ((tree.feature, np.int32), (tree.threshold, np.float64),
+                                                          (tree.left, np.int32), (tree.right, np.int32),
+                                                          (tree.leaf_class, np.int32))]
+    c2v = np.ascontiguousarray(variants, dtype=np.int32)
+    ptrs = [a.ctypes.data_as(ctypes.POINTER(ctypes.c_double if a.dtype == np.float64 else ctypes.c_int32))
+            for a in arrs]
+    return lib.kp_dispatch_load(tree.n_nodes, *ptrs, len(c2v), c2v.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_c_table_routes_like_predict_tree(lib, seed):
+    tree = _random_tree(seed)
+    variants = [lib.kp_family_variant(_lib.FAMILY_SIMT, i * 7) for i in range(5)]
+    h = _load(lib, tree, variants)
+    assert h >= 0
+    rng = np.random.default_rng(100 + seed)
+    dims = rng.integers(1, 1 << 15, size=(20000, 4))
+    feats = np.log2(dims.astype(np.float64))
+    want = predict_tree_batch(tree, feats)
+    got = np.empty(len(feats), dtype=np.int64)
+    buf = np.empty(4, dtype=np.float64)
+    p = buf.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    for i, f in enumerate(feats):
+        buf[:] = f
+        got[i] = lib.kp_dispatch_class_feats(h, p)
+    assert np.array_equal(got, want)
+    # variant ids through the class map, and the C-log2 convenience entry point
+    for i in range(0, 2000, 97):
+        buf[:] = feats[i]
+        assert lib.kp_dispatch_select_feats(h, p) == variants[want[i]]
+        m, k, n, b = (int(v) for v in dims[i])
+        assert lib.kp_dispatch_select(h, m, k, n, b) == variants[predict_tree(tree, np.log2([m, k, n, b]))]
+    assert lib.kp_dispatch_free(h) == 0
+    assert lib.kp_dispatch_class_feats(h, p) == _lib.KP_ENOENT
+
+
+def test_dispatch_load_rejects_malformed_trees(lib):
+    tree = _random_tree(5, n_classes=3)
+    good = [lib.kp_family_variant(_lib.FAMILY_PAPER, i) for i in range(3)]
+    assert _load(lib, tree, [good[0], good[1], 10 ** 6]) == _lib.KP_ENOENT
+    bad = type(tree)(tree.feature, tree.threshold, tree.left.copy(), tree.right, tree.leaf_class)
+    internal = int(np.flatnonzero(tree.leaf_class < 0)[0])
+    bad.left[internal] = 0  # cycle back to the root
+    assert _load(lib, bad, good) == _lib.KP_EINVAL
+    assert b"not a tree" in lib.kp_last_error() or b"reachable" in lib.kp_last_error()
+    assert _load(lib, tree, good[:2]) == _lib.KP_EINVAL  # leaf class outside the class map

@@ -1,0 +1,50 @@
+"""GPU: the tree-dispatched GEMM (C dispatch table -> kp_gemm) launches exactly the
+variant predict_tree names and produces that variant's (bit-exact) result; the CUDA
+event sweep fills every cell of a small table with a positive GFLOP/s."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import gemm_oracle as go
+from paper_2008_13145_b200 import classify, dataset, gemm, selection
+from paper_2008_13145_b200.codegen import export_model
+from paper_2008_13145_b200.dispatch import Dispatcher
+from paper_2008_13145_b200.normalize import NormScheme, normalize
+from paper_2008_13145_b200.sweep import CudaEventTimer, benchmark_sweep
+
+pytestmark = pytest.mark.gpu
+
+
+def test_sweep_every_config_positive(cuda_device):
+    problems = [dataset.ProblemSize(37, 27, 61, 1), dataset.ProblemSize(256, 256, 256, 1),
+                dataset.ProblemSize(1, 1000, 100, 1)]
+    for family in ("simt", "paper"):
+        timer = CudaEventTimer(family, problems, min_ms=0.05, max_iters=20)
+        pm = benchmark_sweep(problems, timer=timer)
+        assert pm.n_configs == 640 and (pm.values > 0).all()
+        assert pm.configs == tuple(dataset.enumerate_configs())
+
+
+def test_dispatcher_matches_predict_tree_and_oracle(cuda_device):
+    problems = [dataset.ProblemSize(m, k, n, 1) for m, k, n in
+                ((64, 64, 64), (512, 512, 512), (1, 2048, 512), (3136, 64, 64), (49, 4608, 512), (1000, 27, 64))]
+    timer = CudaEventTimer("simt", problems, min_ms=0.2)
+    pm = benchmark_sweep(problems, timer=timer)
+    nm = normalize(pm, NormScheme("scaled"))
+    subset = selection.select_subset("kmeans", nm, 4, 0)
+    labels = classify.label_best_in_subset(nm, subset)
+    tree = classify.train_tree(classify.problem_features(pm.problems), labels, classify.TREE_PRESETS["A"],
+                               n_classes=subset.k_actual)
+    disp = Dispatcher(tree, subset, pm.configs, "simt")
+    disp2 = Dispatcher.from_kptree(export_model(tree, subset, pm.configs), "simt")
+    rng = np.random.default_rng(3)
+    for p in problems + [dataset.ProblemSize(300, 100, 70, 1)]:
+        cls = classify.predict_tree(tree, classify.problem_features([p])[0])
+        want_cfg = pm.configs[subset.config_indices[cls]]
+        assert disp.select(p) == want_cfg == disp2.select(p)
+        assert disp.select_c_log2(p) == gemm.variant_id(want_cfg, "simt")
+        A = rng.uniform(-1, 1, (p.m, p.k)).astype(np.float32)
+        B = rng.uniform(-1, 1, (p.k, p.n)).astype(np.float32)
+        got = disp.matmul(torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)).cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), go.gemm_chain(A, B)[0].view(np.uint32))

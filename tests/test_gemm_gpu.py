@@ -1,0 +1,113 @@
+"""GPU parity of the fp32 SIMT families against the CPU oracle (oracle/gemm_ref.c).
+
+Every output element of F0 (paper) and F1 (simt) is the sequential fp32 fma chain
+over k, so the GPU result must equal the oracle BIT FOR BIT -- for every one of the
+640 configs of both families, on aligned and ragged/unaligned shapes (k = 27 and 147
+as in VGG conv1_1 and ResNet conv1), batched and weight-broadcast.  At full sizes the
+check is size-independent: |C - C64| <= 2*k*u*(|A||B|) against a float64 product.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import gemm_oracle as go
+from paper_2008_13145_b200 import gemm
+from paper_2008_13145_b200.dataset import KernelConfig, enumerate_configs
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = enumerate_configs()
+
+
+def _pair(m, k, n, batch, seed=0, bcast=False):
+    rng = np.random.default_rng(seed)
+    A = rng.uniform(-1, 1, (batch, m, k)).astype(np.float32)
+    B = rng.uniform(-1, 1, (k, n) if bcast else (batch, k, n)).astype(np.float32)
+    return A, B
+
+
+def _bits(x):
+    return np.ascontiguousarray(x).view(np.uint32)
+
+
+@pytest.mark.parametrize("family", ["paper", "simt"])
+@pytest.mark.parametrize("shape", [(37, 27, 61, 3), (64, 128, 96, 1), (33, 147, 70, 2)])
+def test_all_640_configs_bit_exact(cuda_device, family, shape):
+    A, B = _pair(*shape)
+    want = _bits(go.gemm_chain(A, B))
+    dA, dB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    bad = []
+    for cfg in CONFIGS:
+        got = gemm.matmul(dA, dB, cfg, family).cpu().numpy()
+        if not np.array_equal(_bits(got), want):
+            bad.append(cfg.as_tuple())
+    assert not bad, f"{len(bad)} configs differ, e.g. {bad[:5]}"
+
+
+EDGE = [1, 7, 31, 64, 255, 256, 1000]
+
+
+@pytest.mark.parametrize("family", ["paper", "simt"])
+@pytest.mark.parametrize("m,k,n", [(m, k, n) for m in EDGE for k in (1, 31, 256) for n in (1, 64, 255)][::3])
+def test_edge_shapes_bit_exact(cuda_device, family, m, k, n):
+    A, B = _pair(m, k, n, 1, seed=m + k + n)
+    want = _bits(go.gemm_chain(A, B))
+    dA, dB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    for cfg in (KernelConfig(8, 4, 8, 16, 16), KernelConfig(1, 1, 1, 1, 64), KernelConfig(4, 8, 2, 128, 1),
+                KernelConfig(2, 2, 8, 8, 32), KernelConfig(8, 1, 4, 64, 1)):
+        assert np.array_equal(_bits(gemm.matmul(dA, dB, cfg, family).cpu().numpy()), want), cfg
+
+
+@pytest.mark.parametrize("family", ["paper", "simt"])
+def test_broadcast_weights_and_strided_views(cuda_device, family):
+    A, W = _pair(50, 72, 40, 4, seed=7, bcast=True)
+    want = _bits(go.gemm_chain(A, W))
+    dA, dW = torch.from_numpy(A).to(cuda_device), torch.from_numpy(W).to(cuda_device)
+    cfg = KernelConfig(4, 4, 4, 16, 16)
+    assert np.array_equal(_bits(gemm.matmul(dA, dW, cfg, family).cpu().numpy()), want)
+    # lda > k and ldb > n: operate on column slices of wider buffers
+    big = torch.from_numpy(np.pad(A, ((0, 0), (0, 0), (0, 5)))).to(cuda_device)[:, :, :72]
+    bigW = torch.from_numpy(np.pad(W, ((0, 0), (0, 3)))).to(cuda_device)[:, :40]
+    out = torch.full((4, 50, 44), 7.0, device=cuda_device)[:, :, :40]
+    gemm.matmul(big, bigW, cfg, family, out=out)
+    assert np.array_equal(_bits(out.cpu().numpy()), want)
+
+
+@pytest.mark.parametrize("family,cfg", [("simt", KernelConfig(8, 4, 8, 16, 16)), ("simt", KernelConfig(8, 2, 8, 8, 16)),
+                                        ("paper", KernelConfig(4, 4, 4, 16, 16))])
+def test_full_size_error_bound(cuda_device, family, cfg):
+    """4096^3 (BASELINE config 5 scale): fp32 bound vs a float64 GPU product."""
+    g = torch.Generator(device=cuda_device).manual_seed(0)
+    n = 4096
+    A = torch.rand(n, n, device=cuda_device, generator=g) * 2 - 1
+    B = torch.rand(n, n, device=cuda_device, generator=g) * 2 - 1
+    C = gemm.matmul(A, B, cfg, family).double()
+    ref = A.double() @ B.double()
+    mag = A.double().abs() @ B.double().abs()
+    assert bool(((C - ref).abs() <= 2 * n * 2.0 ** -24 * mag).all())
+    rel = ((C - ref).norm() / ref.norm()).item()
+    assert rel < 1e-5
+
+
+def test_families_agree_bitwise_at_scale(cuda_device):
+    g = torch.Generator(device=cuda_device).manual_seed(1)
+    A = torch.rand(1000, 2304, device=cuda_device, generator=g)
+    B = torch.rand(2304, 520, device=cuda_device, generator=g)
+    ref = gemm.matmul(A, B, KernelConfig(8, 4, 8, 16, 16), "simt")
+    for fam, cfg in (("paper", KernelConfig(2, 4, 4, 8, 8)), ("simt", KernelConfig(4, 2, 8, 32, 8)),
+                     ("simt", KernelConfig(1, 8, 8, 1, 128))):
+        assert torch.equal(gemm.matmul(A, B, cfg, fam), ref)
+
+
+def test_bad_operands_raise(cuda_device):
+    A = torch.rand(8, 4, device=cuda_device)
+    cfg = KernelConfig(1, 1, 1, 8, 8)
+    with pytest.raises(ValueError):
+        gemm.matmul(A, torch.rand(5, 3, device=cuda_device), cfg)
+    with pytest.raises(ValueError):
+        gemm.matmul(A.double(), torch.rand(4, 3, device=cuda_device).double(), cfg)
+    with pytest.raises(ValueError):
+        gemm.matmul(A.cpu(), torch.rand(4, 3), cfg)
+    with pytest.raises(KeyError):
+        gemm.matmul(A, torch.rand(4, 3, device=cuda_device), KernelConfig(3, 1, 1, 8, 8))

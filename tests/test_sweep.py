@@ -1,0 +1,86 @@
+"""Sweep harness host logic on CPU with the fake hardware timer (the reference's
+SynthModel, dataset.py:147-170): LPT sharding, canonical merge independent of
+scheduling, multi-process (G=2) == serial, resumable partial files, and the merged CSV
+is the reference wire format (dataset.py:36, :206-278)."""
+
+import numpy as np
+import pytest
+
+from paper_2008_13145_b200 import shapes, sweep
+from paper_2008_13145_b200.dataset import (PerfMatrix, ProblemSize, SynthModel, enumerate_configs,
+                                           parse_benchmark_csv, serialize_benchmark_csv, synth_generate)
+
+CFGS = tuple(enumerate_configs()[:40])
+PROBS = shapes.network_problems("vgg16", batches=(1, 2, 4))
+
+
+def test_lpt_shards_partition_and_balance():
+    shards = sweep.lpt_shards(PROBS, 3)
+    flat = sorted(i for s in shards for i in s)
+    assert flat == list(range(len(PROBS)))
+    loads = [sum(PROBS[i].flops for i in s) for s in shards]
+    assert max(loads) <= 1.6 * (sum(loads) / 3) + max(p.flops for p in PROBS)
+    assert sweep.lpt_shards(PROBS, 3) == shards  # deterministic
+    with pytest.raises(ValueError):
+        sweep.lpt_shards(PROBS, 0)
+
+
+def test_serial_sweep_equals_synth_generate():
+    timer = sweep.SynthTimer(CFGS, SynthModel())
+    pm = sweep.benchmark_sweep(PROBS, timer=timer, configs=CFGS)
+    assert pm == synth_generate(SynthModel(), PROBS, list(CFGS))
+
+
+def test_two_process_sweep_equals_serial(tmp_path):
+    serial = sweep.benchmark_sweep(PROBS, timer=sweep.SynthTimer(CFGS, SynthModel()), configs=CFGS)
+    par = sweep.benchmark_sweep(PROBS, gpus=2, out_dir=tmp_path, timer_kind="synth",
+                                timer_kw={"configs": CFGS, "model": SynthModel()}, configs=CFGS)
+    assert par == serial
+    assert (tmp_path / "shard0.csv").exists() and (tmp_path / "shard1.csv").exists()
+    text = serialize_benchmark_csv(par)
+    assert parse_benchmark_csv(text) == par
+
+
+def test_resume_skips_measured_cells(tmp_path):
+    calls = []
+
+    class Counting(sweep.SynthTimer):
+        def __call__(self, problem, ci):
+            calls.append((problem, ci))
+            return super().__call__(problem, ci)
+
+    first = sweep.benchmark_sweep(PROBS[:3], timer=Counting(CFGS), configs=CFGS, out_dir=tmp_path)
+    n_first = len(calls)
+    assert n_first == 3 * len(CFGS)
+    again = sweep.benchmark_sweep(PROBS[:4], timer=Counting(CFGS), configs=CFGS, out_dir=tmp_path)
+    assert len(calls) - n_first == len(CFGS)  # only the new row was measured
+    assert again.take_rows(range(3)) == first
+
+
+def test_failed_cell_is_fatal():
+    def broken(problem, ci):
+        return (0.0, 1.0, 1)
+    broken.configs = CFGS
+    with pytest.raises(Exception):
+        sweep.benchmark_sweep(PROBS[:1], timer=broken, configs=CFGS)
+
+
+def test_reference_parses_sweep_csv(kernelprune_ref, tmp_path):
+    pm = sweep.benchmark_sweep(PROBS, timer=sweep.SynthTimer(CFGS, SynthModel(noise_sigma=0.0)), configs=CFGS)
+    path = tmp_path / "t.csv"
+    sweep.write_benchmark_csv(pm, path)
+    ref = kernelprune_ref["dataset"].parse_benchmark_csv(path.read_text())
+    assert [p.__dict__ for p in ref.problems] == [p.__dict__ for p in pm.problems]
+    assert np.array_equal(ref.values, pm.values)
+
+
+def test_shape_sets():
+    vgg = shapes.network_problems("vgg16", batches=(1,))
+    assert len(vgg) == 12
+    assert shapes.network_flops("vgg16", 1) == pytest.approx(30.94e9, rel=0.01)
+    res = shapes.network_problems("resnet50", batches=(1,))
+    assert len(res) == 21
+    assert shapes.network_flops("resnet50", 1) == pytest.approx(8.18e9, rel=0.02)
+    allv = shapes.network_problems("vgg16")
+    assert len(allv) == len(set(allv))
+    assert ProblemSize(784, 4608, 512, 1) in allv  # conv4_2 @1 == conv5 @4 kept once

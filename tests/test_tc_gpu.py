@@ -1,0 +1,60 @@
+"""GPU: the tcgen05 tensor-core families (F2 TF32, F3 BF16) against a float64
+product of the same (tf32-truncated / bf16) operands.
+
+Stated tolerances (widened for TF32 truncation: tcgen05 kind::tf32
+reads the top 19 bits of each fp32 operand):
+    TF32: |C - C64| <= (2 * 2^-10 + 2*k*2^-24) * (|A||B|)_ij
+    BF16: |C - C64| <= (2*k*2^-24) * (|A_bf16||B_bf16|)_ij  (inputs exact in bf16)
+"""
+
+import pytest
+import torch
+
+from paper_2008_13145_b200 import gemm
+from paper_2008_13145_b200.dataset import KernelConfig
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -24
+
+
+def _check(fam, cfg, m, k, n, batch, dev, bcast=False, seed=0):
+    g = torch.Generator(device=dev).manual_seed(seed)
+    A = torch.rand(batch, m, k, device=dev, generator=g) * 2 - 1
+    B = torch.rand(k, n, device=dev, generator=g) * 2 - 1
+    if not bcast:
+        B = B.expand(batch, k, n).contiguous() + torch.rand(batch, k, n, device=dev, generator=g) * 0.1
+    if fam == "bf16":
+        A, B = A.bfloat16(), B.bfloat16()
+        A64, B64 = A.double(), B.double()
+        eps_in = 0.0
+    else:
+        A64, B64 = A.double(), B.double()
+        eps_in = 2.0 * 2.0 ** -10
+    C = gemm.matmul(A, B, cfg, fam).double()
+    ref = A64 @ B64
+    mag = A64.abs() @ B64.abs()
+    bound = (eps_in + 2 * k * U) * mag + 1e-30
+    worst = ((C - ref).abs() / bound).max().item()
+    assert worst <= 1.0, f"{fam} {cfg.as_tuple()} {m}x{k}x{n}x{batch}: error {worst:.3f} x bound"
+
+
+@pytest.mark.parametrize("fam", ["bf16", "tf32"])
+def test_every_config_square(cuda_device, fam):
+    for cfg in gemm.family_configs(fam):
+        _check(fam, cfg, 256, 256, 256, 1, cuda_device)
+
+
+@pytest.mark.parametrize("fam", ["bf16", "tf32"])
+@pytest.mark.parametrize("m,k,n,batch", [(1, 64, 64, 1), (130, 72, 200, 1), (1000, 576, 64, 2), (49, 4608, 512, 1),
+                                         (333, 1000, 1000, 1), (16, 8, 8, 3), (2048, 2048, 2048, 1)])
+def test_ragged_and_batched(cuda_device, fam, m, k, n, batch):
+    for cfg in gemm.family_configs(fam)[::3]:
+        _check(fam, cfg, m, k, n, batch, cuda_device, bcast=(batch > 1), seed=m + n)
+
+
+def test_unaligned_leading_dim_is_rejected(cuda_device):
+    A = torch.rand(64, 27, device=cuda_device).bfloat16()
+    B = torch.rand(27, 64, device=cuda_device).bfloat16()
+    with pytest.raises(ValueError):
+        gemm.matmul(A, B, gemm.family_configs("bf16")[0], "bf16")
