@@ -90,6 +90,17 @@ int kp_gemm(int id, int m, int k, int n, int batch,
             const void* B, int64_t ldb, int64_t sB,
             void* C, int64_t ldc, int64_t sC, void* stream);
 
+/* Fused epilogue variant (VGG16 conv/fc layers):
+ *   C = act(A * B + bias[col]), bias may be NULL, act = ReLU when flags & KP_EPI_RELU.
+ * The bias add and ReLU follow the fp32 accumulation chain, so SIMT results stay
+ * bit-exact against oracle_chain + bias -> max(0, .). */
+#define KP_EPI_RELU 1
+int kp_gemm_ex(int id, int m, int k, int n, int batch,
+               const void* A, int64_t lda, int64_t sA,
+               const void* B, int64_t ldb, int64_t sB,
+               void* C, int64_t ldc, int64_t sC,
+               const float* bias, int flags, void* stream);
+
 /* ---- benchmark harness ---------------------------------------------------
  * warmup untimed launches, then one launch timed alone to size the loop, then
  * max(min_iters, ceil(min_ms / t1)) (capped at max_iters) back-to-back launches
@@ -131,6 +142,19 @@ int kp_gemm_auto(int handle, int m, int k, int n, int batch,
                  const void* A, int64_t lda, int64_t sA,
                  const void* B, int64_t ldb, int64_t sB,
                  void* C, int64_t ldc, int64_t sC, void* stream, int* variant_out);
+int kp_gemm_auto_ex(int handle, int m, int k, int n, int batch,
+                    const void* A, int64_t lda, int64_t sA,
+                    const void* B, int64_t ldb, int64_t sB,
+                    void* C, int64_t ldc, int64_t sC,
+                    const float* bias, int flags, void* stream, int* variant_out);
+
+/* ---- conv-as-GEMM helpers for VGG16 inference (NHWC fp32) ----------------
+ * im2col of a 3x3, stride 1, pad 1 convolution: x is (B, H, W, C); out row
+ * r = (b*H + h)*W + w holds the 9*C patch values ordered (dy, dx, c) -- the k order of
+ * the (9*C) x Cout weight matrix -- with zeros outside the image; ldo >= 9*C. */
+int kp_im2col3x3_nhwc(const float* x, int B, int H, int W, int C, float* out, int64_t ldo, void* stream);
+/* 2x2 / stride 2 max pooling, NHWC: (B, H, W, C) -> (B, H/2, W/2, C). */
+int kp_maxpool2x2_nhwc(const float* x, int B, int H, int W, int C, float* out, void* stream);
 
 #ifdef __cplusplus
 }

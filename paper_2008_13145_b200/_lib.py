@@ -22,6 +22,7 @@ KP_OK = 0
 KP_ENOENT = -2
 KP_EIO = -5
 KP_EINVAL = -22
+KP_EPI_RELU = 1
 
 FAMILY_PAPER = 0
 FAMILY_SIMT = 1
@@ -66,6 +67,7 @@ SIGNATURES = {
     "kp_family_size": (_i, [_i]),
     "kp_family_variant": (_i, [_i, _i]),
     "kp_gemm": (_i, [_i] + _GEMM_ARGS + [_vp]),
+    "kp_gemm_ex": (_i, [_i] + _GEMM_ARGS + [_vp, _i, _vp]),
     "kp_bench": (_i, [_i] + _GEMM_ARGS + [_i, _i, _i, ctypes.c_double, _dp, _ip, _vp]),
     "kp_ffma_peak": (_i, [_i, _dp, _vp]),
     "kp_dispatch_load": (_i, [_i, _i32p, _dp, _i32p, _i32p, _i32p, _i, _i32p]),
@@ -74,6 +76,9 @@ SIGNATURES = {
     "kp_dispatch_select_feats": (_i, [_i, _dp]),
     "kp_dispatch_select": (_i, [_i, _i, _i, _i, _i]),
     "kp_gemm_auto": (_i, [_i] + _GEMM_ARGS + [_vp, _ip]),
+    "kp_gemm_auto_ex": (_i, [_i] + _GEMM_ARGS + [_vp, _i, _vp, _ip]),
+    "kp_im2col3x3_nhwc": (_i, [_vp, _i, _i, _i, _i, _vp, _i64, _vp]),
+    "kp_maxpool2x2_nhwc": (_i, [_vp, _i, _i, _i, _i, _vp, _vp]),
 }
 
 _lock = threading.Lock()

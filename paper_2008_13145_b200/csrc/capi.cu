@@ -130,6 +130,8 @@ kp::GemmArgs make_args(int m, int k, int n, int batch, const void* A, int64_t ld
   p.B = B; p.ldb = ldb; p.sB = sB;
   p.C = C; p.ldc = ldc; p.sC = sC;
   p.a_vec = p.b_vec = p.c_vec = 0;
+  p.bias = nullptr;
+  p.relu = 0;
   return p;
 }
 
@@ -205,6 +207,18 @@ int kp_gemm(int id, int m, int k, int n, int batch, const void* A, int64_t lda, 
   int rc = check_problem(id, m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC);
   if (rc != KP_OK) return rc;
   return launch(id, make_args(m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC), static_cast<cudaStream_t>(stream));
+}
+
+int kp_gemm_ex(int id, int m, int k, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* B,
+               int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, const float* bias, int flags,
+               void* stream) {
+  int rc = check_problem(id, m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC);
+  if (rc != KP_OK) return rc;
+  if (flags & ~KP_EPI_RELU) return fail(KP_EINVAL, "unknown epilogue flags 0x%x", flags);
+  kp::GemmArgs p = make_args(m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC);
+  p.bias = bias;
+  p.relu = (flags & KP_EPI_RELU) != 0;
+  return launch(id, p, static_cast<cudaStream_t>(stream));
 }
 
 int kp_bench(int id, int m, int k, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* B,
@@ -289,6 +303,21 @@ int kp_ffma_peak(int packed, double* tflops, void* stream) {
   return KP_OK;
 }
 
+int kp_im2col3x3_nhwc(const float* x, int B, int H, int W, int C, float* out, int64_t ldo, void* stream) {
+  if (!x || !out) return fail(KP_EINVAL, "null pointer");
+  if (B < 1 || H < 1 || W < 1 || C < 1) return fail(KP_EINVAL, "bad activation shape");
+  if (ldo < 9LL * C) return fail(KP_EINVAL, "ldo smaller than 9*C");
+  cudaError_t e = kp::im2col3x3_nhwc_launch(x, B, H, W, C, out, ldo, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? KP_OK : cuda_fail(e, "im2col launch");
+}
+
+int kp_maxpool2x2_nhwc(const float* x, int B, int H, int W, int C, float* out, void* stream) {
+  if (!x || !out) return fail(KP_EINVAL, "null pointer");
+  if (B < 1 || H < 2 || W < 2 || C < 1) return fail(KP_EINVAL, "bad activation shape");
+  cudaError_t e = kp::maxpool2_nhwc_launch(x, B, H, W, C, out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? KP_OK : cuda_fail(e, "maxpool launch");
+}
+
 int kp_dispatch_load(int n_nodes, const int32_t* feature, const double* threshold, const int32_t* left,
                      const int32_t* right, const int32_t* leaf_class, int n_classes,
                      const int32_t* class_to_variant) {
@@ -364,10 +393,17 @@ int kp_dispatch_select(int handle, int m, int k, int n, int batch) {
 
 int kp_gemm_auto(int handle, int m, int k, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* B,
                  int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, void* stream, int* variant_out) {
+  return kp_gemm_auto_ex(handle, m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC, nullptr, 0, stream,
+                         variant_out);
+}
+
+int kp_gemm_auto_ex(int handle, int m, int k, int n, int batch, const void* A, int64_t lda, int64_t sA,
+                    const void* B, int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, const float* bias,
+                    int flags, void* stream, int* variant_out) {
   const int id = kp_dispatch_select(handle, m, k, n, batch);
   if (id < 0) return id;
   if (variant_out) *variant_out = id;
-  return kp_gemm(id, m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC, stream);
+  return kp_gemm_ex(id, m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC, bias, flags, stream);
 }
 
 }  // extern "C"

@@ -22,7 +22,18 @@ struct GemmArgs {
   int a_vec;  // rows of A may be read with the family's vector width along k
   int b_vec;  // rows of B may be read with the family's vector width along n
   int c_vec;  // rows of C may be written with the family's vector width along n
+  // Fused epilogue (kp_gemm_ex): C = act(A*B + bias[col]); bias may be null.
+  const float* bias;
+  int relu;
 };
+
+// Epilogue of every family: bias add (fp32, round-to-nearest) then ReLU.  Applied
+// after the fma chain, so the result equals oracle_chain + bias -> max(0, .) exactly.
+__device__ __forceinline__ float epilogue(const GemmArgs& p, float v, int64_t col) {
+  if (p.bias) v = v + __ldg(p.bias + col);
+  if (p.relu) v = fmaxf(v, 0.0f);
+  return v;
+}
 
 // ---- vector load / store of N consecutive floats (N in {1,2,4,8}) ---------
 template <int N>

@@ -98,6 +98,13 @@ __global__ void f0_kernel(GemmArgs p, int groups_n) {
         for (int c = 0; c < C; ++c) acc[r][c] = __fmaf_rn(a[r][i], w[i][c], acc[r][c]);
   }
 
+  if (p.bias || p.relu) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        if (col0 + c < n) acc[r][c] = epilogue(p, acc[r][c], col0 + c);
+  }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     if (!rows_full && row0 + r >= m) break;

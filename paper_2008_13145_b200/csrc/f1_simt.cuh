@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
       for (int e = 0; e < VC; ++e) {
         const float2 pr = acc[r][(cv * VC + e) / 2];
         v[e] = ((cv * VC + e) & 1) ? pr.y : pr.x;
+        if (p.bias || p.relu) v[e] = (col + e < n) ? epilogue(p, v[e], col + e) : v[e];
       }
       if (p.c_vec && col + VC <= n) {
         stg_vec<VC>(out + col, v);

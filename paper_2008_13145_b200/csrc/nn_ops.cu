@@ -1,0 +1,79 @@
+// Conv-as-GEMM helpers for VGG16 inference (BASELINE.json configs[2]), NHWC fp32.
+//
+// The paper evaluates its selected kernels inside a VGG16 network
+// where SYCL-DNN lowers convolutions to matmuls.  Here a 3x3 / stride 1 / pad 1
+// convolution becomes im2col (this kernel) + one tree-dispatched GEMM with the bias
+// and ReLU fused into the GEMM epilogue (kp_gemm_ex); pooling is a separate HBM-bound
+// pass.  NHWC keeps the GEMM output (B*H*W) x Cout equal to the next layer's input.
+#include "families.h"
+
+namespace kp {
+namespace {
+
+// One thread per output element; consecutive threads walk k = (dy*3 + dx)*C + c, so
+// both the gather (contiguous channels of one tap) and the store are coalesced.
+__global__ void im2col3x3_nhwc_kernel(const float* __restrict__ x, int B, int H, int W, int C,
+                                      float* __restrict__ out, int64_t ldo) {
+  const int64_t K = 9LL * C;
+  const int64_t total = static_cast<int64_t>(B) * H * W * K;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / K;
+    const int kk = static_cast<int>(i - row * K);
+    const int tap = kk / C, c = kk - tap * C;
+    const int dy = tap / 3 - 1, dx = tap % 3 - 1;
+    const int w = static_cast<int>(row % W);
+    const int64_t bh = row / W;
+    const int h = static_cast<int>(bh % H);
+    const int b = static_cast<int>(bh / H);
+    const int hy = h + dy, wx = w + dx;
+    float v = 0.0f;
+    if (hy >= 0 && hy < H && wx >= 0 && wx < W) v = __ldg(x + ((static_cast<int64_t>(b) * H + hy) * W + wx) * C + c);
+    out[row * ldo + kk] = v;
+  }
+}
+
+// 2x2 / stride 2 max pool; one thread per output element (channel fastest).
+__global__ void maxpool2_nhwc_kernel(const float* __restrict__ x, int B, int H, int W, int C, float* __restrict__ out) {
+  const int Ho = H / 2, Wo = W / 2;
+  const int64_t total = static_cast<int64_t>(B) * Ho * Wo * C;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    int64_t r = i / C;
+    const int wo = static_cast<int>(r % Wo);
+    r /= Wo;
+    const int ho = static_cast<int>(r % Ho);
+    const int64_t b = r / Ho;
+    const float* base = x + ((b * H + 2 * ho) * W + 2 * wo) * C + c;
+    const float a0 = __ldg(base), a1 = __ldg(base + C);
+    const float a2 = __ldg(base + static_cast<int64_t>(W) * C), a3 = __ldg(base + static_cast<int64_t>(W) * C + C);
+    out[i] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+  }
+}
+
+int grid_for(int64_t total, int threads) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (total + threads - 1) / threads;
+  const int64_t cap = static_cast<int64_t>(sms) * 32;  // grid-stride beyond 32 CTAs/SM
+  return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+}  // namespace
+
+cudaError_t im2col3x3_nhwc_launch(const float* x, int B, int H, int W, int C, float* out, int64_t ldo,
+                                  cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(B) * H * W * 9 * C;
+  im2col3x3_nhwc_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, B, H, W, C, out, ldo);
+  return cudaGetLastError();
+}
+
+cudaError_t maxpool2_nhwc_launch(const float* x, int B, int H, int W, int C, float* out, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(B) * (H / 2) * (W / 2) * C;
+  maxpool2_nhwc_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, B, H, W, C, out);
+  return cudaGetLastError();
+}
+
+}  // namespace kp

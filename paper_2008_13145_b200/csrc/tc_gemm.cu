@@ -213,6 +213,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + c, v);
       if (row < p.m) {
         const int col = n0 + c;
+        if (p.bias || p.relu) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (col + e < p.n) v[e] = epilogue(p, v[e], col + e);
+        }
         if (p.c_vec && col + 16 <= p.n) {
 #pragma unroll
           for (int q = 0; q < 4; ++q)

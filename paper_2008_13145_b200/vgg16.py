@@ -1,0 +1,146 @@
+"""VGG16 inference with tree-dispatched GEMMs (BASELINE.json configs[2]; the paper's
+system-level check).
+
+Every convolution is 3x3 / stride 1 / pad 1 and runs as im2col (``kp_im2col3x3_nhwc``)
++ one GEMM (m = B*H*W, k = 9*Cin, n = Cout) launched through the C dispatch table with
+the bias add and ReLU fused into the GEMM epilogue (``kp_gemm_ex``); 2x2 max pooling
+is ``kp_maxpool2x2_nhwc``; fc6/fc7/fc8 are GEMMs with m = B.  Activations are NHWC
+fp32, so each GEMM output is directly the next layer's input.  Weights are He-normal
+random (no network access for trained weights), seeded, identical on every rank.
+
+Data parallelism (configs[2] at 1/2/4/8 GPUs): each rank runs its own images with
+replicated weights; there is no collective on the data path.  The whole forward for a
+fixed batch can be captured once in a CUDA graph (``Vgg16.capture``) because all
+buffers are preallocated.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from .dataset import ProblemSize
+
+# (Cin, Cout) per conv, "M" = 2x2 max pool (configuration D).
+VGG16_PLAN = ((3, 64), (64, 64), "M", (64, 128), (128, 128), "M", (128, 256), (256, 256), (256, 256), "M",
+              (256, 512), (512, 512), (512, 512), "M", (512, 512), (512, 512), (512, 512), "M")
+VGG16_FC = ((7 * 7 * 512, 4096, True), (4096, 4096, True), (4096, 1000, False))
+
+
+def init_weights(seed: int = 0, device="cpu"):
+    """He-normal conv/fc weights ((9*Cin) x Cout / in x out, row-major) and small
+    biases, deterministic for a seed (generated on CPU so every device agrees)."""
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    convs, fcs = [], []
+    for item in VGG16_PLAN:
+        if item == "M":
+            continue
+        cin, cout = item
+        w = torch.randn(9 * cin, cout, generator=g) * math.sqrt(2.0 / (9 * cin))
+        b = torch.randn(cout, generator=g) * 0.01
+        convs.append((w.to(device), b.to(device)))
+    for fin, fout, _ in VGG16_FC:
+        w = torch.randn(fin, fout, generator=g) * math.sqrt(2.0 / fin)
+        b = torch.randn(fout, generator=g) * 0.01
+        fcs.append((w.to(device), b.to(device)))
+    return convs, fcs
+
+
+class Vgg16:
+    """Preallocated VGG16 forward for a fixed batch on one device."""
+
+    def __init__(self, dispatcher, batch: int, device, seed: int = 0, weights=None):
+        self.disp = dispatcher
+        self.batch = batch
+        self.device = torch.device(device)
+        convs, fcs = weights if weights is not None else init_weights(seed)
+        self.convs = [(w.to(self.device).contiguous(), b.to(self.device).contiguous()) for w, b in convs]
+        self.fcs = [(w.to(self.device).contiguous(), b.to(self.device).contiguous()) for w, b in fcs]
+        B = batch
+        # ping-pong activation buffers sized for the largest layer output (B*224*224*64)
+        act = B * 224 * 224 * 64
+        self.act = [torch.empty(act, device=self.device) for _ in range(2)]
+        self.cols = torch.empty(B * 224 * 224 * 9 * 64, device=self.device)  # conv1_2 im2col
+        self.input = torch.empty(B, 224, 224, 3, device=self.device)
+        self.logits = torch.empty(B, 1000, device=self.device)
+        self.fc_buf = [torch.empty(B, 4096, device=self.device) for _ in range(2)]
+        self.launches = []  # (problem, variant) per GEMM, filled on first forward
+        self.graph = None
+
+    def problems(self) -> list[ProblemSize]:
+        out, H, B = [], 224, self.batch
+        for item in VGG16_PLAN:
+            if item == "M":
+                H //= 2
+                continue
+            cin, cout = item
+            out.append(ProblemSize(B * H * H, 9 * cin, cout, 1))
+        out += [ProblemSize(B, fin, fout, 1) for fin, fout, _ in VGG16_FC]
+        return out
+
+    def _gemm(self, A, W, bias, C, m, k, n, relu, stream):
+        lib = _lib.load()
+        vid = self.disp.variant(ProblemSize(m, k, n, 1))
+        _lib.check(lib.kp_gemm_ex(vid, m, k, n, 1, A.data_ptr(), k, 0, W.data_ptr(), n, 0, C.data_ptr(), n, 0,
+                                  bias.data_ptr(), _lib.KP_EPI_RELU if relu else 0, stream),
+                   f"kp_gemm_ex({m},{k},{n})")
+        return vid
+
+    def _forward(self, stream_handle):
+        lib = _lib.load()
+        B, H, C = self.batch, 224, 3
+        src = self.input
+        dst_i = 0
+        ci = 0
+        for item in VGG16_PLAN:
+            dst = self.act[dst_i]
+            if item == "M":
+                _lib.check(lib.kp_maxpool2x2_nhwc(src.data_ptr(), B, H, H, C, dst.data_ptr(), stream_handle),
+                           "kp_maxpool2x2_nhwc")
+                H //= 2
+            else:
+                cin, cout = item
+                w, b = self.convs[ci]
+                ci += 1
+                m, k = B * H * H, 9 * cin
+                _lib.check(lib.kp_im2col3x3_nhwc(src.data_ptr(), B, H, H, cin, self.cols.data_ptr(), k,
+                                                 stream_handle), "kp_im2col3x3_nhwc")
+                self._gemm(self.cols, w, b, dst, m, k, cout, True, stream_handle)
+                C = cout
+            src = dst
+            dst_i ^= 1
+        x = src  # (B, 7, 7, 512) NHWC flattened per image = fc6 input rows
+        for j, ((fin, fout, relu), (w, b)) in enumerate(zip(VGG16_FC, self.fcs)):
+            out = self.logits if j == len(self.fcs) - 1 else self.fc_buf[j % 2]
+            self._gemm(x, w, b, out, B, fin, fout, relu, stream_handle)
+            x = out
+        return self.logits
+
+    def forward(self, x: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """x: (B, 224, 224, 3) NHWC fp32 (copied into the input buffer) -> logits (B, 1000)."""
+        stream = stream or torch.cuda.current_stream(self.device)
+        if x is not None:
+            with torch.cuda.stream(stream):
+                self.input.copy_(x, non_blocking=True)
+        if self.graph is not None:
+            with torch.cuda.stream(stream):
+                self.graph.replay()
+            return self.logits
+        return self._forward(stream.cuda_stream)
+
+    def capture(self, stream: torch.cuda.Stream | None = None) -> None:
+        """Capture the whole forward in a CUDA graph (launch-bound small batches)."""
+        stream = stream or torch.cuda.Stream(self.device)
+        with torch.cuda.stream(stream):
+            self._forward(stream.cuda_stream)  # warm: resolves variants, sets kernel attributes
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            self._forward(torch.cuda.current_stream().cuda_stream)
+        self.graph = g
+
+    @property
+    def flops(self) -> int:
+        return sum(p.flops for p in self.problems()) + 0  # GEMM flops (duplicates counted per layer)

@@ -1,0 +1,61 @@
+"""GPU: VGG16 inference (im2col + tree-dispatched GEMMs with fused bias/ReLU + max pool)
+equals the CPU oracle forward (oracle/vgg16_ref.py) bit for bit, eager and as a CUDA
+graph; the conv helpers match their numpy restatements exactly."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import vgg16_ref
+from paper_2008_13145_b200 import _lib, classify, dataset, selection, vgg16
+from paper_2008_13145_b200.dispatch import Dispatcher
+from paper_2008_13145_b200.normalize import NormScheme, normalize
+from paper_2008_13145_b200.sweep import SynthTimer, benchmark_sweep
+
+pytestmark = pytest.mark.gpu
+
+
+def _dispatcher(batch):
+    # a tree over a synthetic table is enough to exercise dispatch of every layer
+    model = vgg16.Vgg16.__new__(vgg16.Vgg16)
+    model.batch = batch
+    probs = list(dict.fromkeys(vgg16.Vgg16.problems(model)))
+    cfgs = tuple(dataset.enumerate_configs())
+    pm = benchmark_sweep(probs, timer=SynthTimer(cfgs), configs=cfgs)
+    nm = normalize(pm, NormScheme())
+    sub = selection.select_subset("kmeans", nm, min(4, len(probs)), 0)
+    labels = classify.label_best_in_subset(nm, sub)
+    tree = classify.train_tree(classify.problem_features(pm.problems), labels, classify.TREE_PRESETS["A"],
+                               n_classes=sub.k_actual)
+    return Dispatcher(tree, sub, pm.configs, "simt")
+
+
+def test_im2col_and_pool_exact(cuda_device):
+    lib = _lib.load()
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((2, 9, 7, 5)).astype(np.float32)
+    dx = torch.from_numpy(x).to(cuda_device)
+    out = torch.empty(2 * 9 * 7, 45, device=cuda_device)
+    assert lib.kp_im2col3x3_nhwc(dx.data_ptr(), 2, 9, 7, 5, out.data_ptr(), 45, None) == 0
+    assert np.array_equal(out.cpu().numpy(), vgg16_ref.im2col3x3(x))
+    y = rng.standard_normal((2, 8, 6, 3)).astype(np.float32)
+    dy = torch.from_numpy(y).to(cuda_device)
+    pout = torch.empty(2, 4, 3, 3, device=cuda_device)
+    assert lib.kp_maxpool2x2_nhwc(dy.data_ptr(), 2, 8, 6, 3, pout.data_ptr(), None) == 0
+    assert np.array_equal(pout.cpu().numpy(), vgg16_ref.maxpool2(y))
+
+
+@pytest.mark.parametrize("batch", [1, 2])
+def test_vgg16_forward_bit_exact(cuda_device, batch):
+    convs, fcs = vgg16.init_weights(seed=0)
+    model = vgg16.Vgg16(_dispatcher(batch), batch, cuda_device, weights=(convs, fcs))
+    g = torch.Generator().manual_seed(7)
+    x = torch.randn(batch, 224, 224, 3, generator=g)
+    got = model.forward(x.to(cuda_device)).cpu().numpy().copy()
+    want = vgg16_ref.forward(x.numpy(), [(w.numpy(), b.numpy()) for w, b in convs],
+                             [(w.numpy(), b.numpy()) for w, b in fcs])
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    model.capture()
+    again = model.forward(x.to(cuda_device)).cpu().numpy()
+    torch.cuda.synchronize()
+    assert np.array_equal(again.view(np.uint32), want.view(np.uint32))

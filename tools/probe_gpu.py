@@ -34,8 +34,9 @@ for shp in [] if PERF_ONLY else [(256, 256, 256, 1), (37, 27, 61, 3), (1, 1000, 
     check(*shp, cfgs)
 
 def tflops(fam, cfg, m, k, n, batch=1):
-    A = torch.rand(batch, m, k, device=dev); B = torch.rand(batch, k, n, device=dev)
-    ops = gemm.GemmOperands(A, B, None, torch.float32)
+    dt = gemm.input_dtype(fam)
+    A = torch.rand(batch, m, k, device=dev).to(dt); B = torch.rand(batch, k, n, device=dev).to(dt)
+    ops = gemm.GemmOperands(A, B, None, dt)
     vid = gemm.variant_id(cfg, fam)
     ms, it = gemm.bench(vid, ops, warmup=2, min_ms=50)
     return 2.0 * m * k * n * batch / (ms * 1e-3) / 1e12
@@ -48,6 +49,32 @@ for N in ((4096, 8192) if PERF_ONLY else (1024, 4096, 8192)):
     for cfg in (KernelConfig(8, 4, 8, 8, 16), KernelConfig(8, 4, 8, 16, 8), KernelConfig(4, 4, 8, 16, 16), KernelConfig(8, 4, 4, 16, 16)):
         res[f"simt{cfg.as_tuple()}@{N}"] = tflops("simt", cfg, N, N, N)
     res[f"paper(4,4,4,16,16)@{N}"] = tflops("paper", KernelConfig(4, 4, 4, 16, 16), N, N, N)
+    for fam in ("bf16", "tf32"):
+        for cfg in gemm.family_configs(fam):
+            try:
+                res[f"{fam}{cfg.as_tuple()}@{N}"] = tflops(fam, cfg, N, N, N)
+            except Exception as exc:  # report and continue
+                print(f"{fam}{cfg.as_tuple()} failed: {exc}", flush=True)
+    for dt, name in ((torch.bfloat16, "cublas_bf16"),):
+        a = torch.rand(N, N, device=dev).to(dt); b = torch.rand(N, N, device=dev).to(dt)
+        for _ in range(3): torch.matmul(a, b)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        reps = max(3, int(2e14 / (2 * N**3)))
+        e0.record()
+        for _ in range(reps): torch.matmul(a, b)
+        e1.record(); torch.cuda.synchronize()
+        res[f"{name}@{N}"] = 2.0 * N**3 * reps / (e0.elapsed_time(e1) * 1e-3) / 1e12
+    torch.backends.cuda.matmul.allow_tf32 = True
+    a = torch.rand(N, N, device=dev); b = torch.rand(N, N, device=dev)
+    for _ in range(3): torch.matmul(a, b)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    reps = max(3, int(1e14 / (2 * N**3)))
+    e0.record()
+    for _ in range(reps): torch.matmul(a, b)
+    e1.record(); torch.cuda.synchronize()
+    res[f"cublas_tf32@{N}"] = 2.0 * N**3 * reps / (e0.elapsed_time(e1) * 1e-3) / 1e12
     res[f"paper(8,4,8,16,16)@{N}"] = tflops("paper", KernelConfig(8, 4, 8, 16, 16), N, N, N)
     torch.backends.cuda.matmul.allow_tf32 = False
     a = torch.rand(N, N, device=dev); b = torch.rand(N, N, device=dev)
