@@ -6,7 +6,9 @@
 //   * TMA (cp.async.bulk.tensor) loads 128-byte-swizzled tiles into a STAGES-deep
 //     shared-memory ring, signalling full/empty mbarriers;
 //   * one elected thread issues tcgen05.mma (M=128, N=BN, K=32 bytes per instruction)
-//     with A K-major and B MN-major (B is row-major K x N, so no transpose pass),
+//     with A K-major and B MN-major (B is row-major K x N, so no transpose pass; for
+//     tf32 the MN-major tile uses the 32-byte-atom 128B swizzle, the only MN-major
+//     32-bit layout UMMA accepts),
 //     accumulating in TMEM (BN fp32 columns x 128 lanes);
 //   * tcgen05.commit frees each smem stage and finally signals the epilogue warps,
 //     which drain TMEM with tcgen05.ld (32x32b) and store fp32 rows.
@@ -17,6 +19,11 @@
 // (tile_rows, tile_acc, tile_cols, wg_rows, wg_cols) =
 //   (BM = 128, BK = elements per 128-byte K slab, BN, STAGES, threads = 192).
 //
+// Operands whose rows are not 16-byte aligned (TMA's requirement; e.g. VGG conv1_1
+// k = 27, ResNet conv1 k = 147) are staged by the epilogue warps with ordinary loads
+// into the identical swizzled layout, so every family runs every shape (the grid
+// must be complete, dataset.py:259-264).
+//
 // Numerics: BF16 operands are exact bf16 inputs, fp32 accumulation.  TF32 reads fp32
 // operands and uses their top 19 bits (truncation), fp32 accumulation; tolerances in
 // tests/test_tc_gpu.py: |C - C64| <= (2*eps_in + 2*k*2^-24) * (|A||B|)_ij.
@@ -24,6 +31,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 
 #include "tc_families.h"
 
@@ -66,14 +74,18 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// Shared-memory matrix descriptor, SWIZZLE_128B, version 1 (sm_100).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+// Shared-memory matrix descriptor, version 1 (sm_100).  layout 2 = SWIZZLE_128B
+// (16-byte chunks XOR row%8 over 1024-byte atoms), layout 1 = SWIZZLE_128B_BASE32B
+// (32-byte chunks XOR row%4 over 512-byte atoms) -- the only MN-major layout the
+// tensor core accepts for 32-bit (tf32) operands.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                              uint32_t layout = 2) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
   d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
   d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
   d |= static_cast<uint64_t>(1) << 46;  // version
-  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  d |= static_cast<uint64_t>(layout) << 61;
   return d;
 }
 
@@ -131,7 +143,40 @@ struct TcCfg {
   static_assert(SMEM_BYTES <= 227 * 1024, "smem");
 };
 
-template <bool kTF32, int BN, int STAGES>
+// LSU staging (operands whose rows are not 16-byte aligned, e.g. k = 27 or 147, so
+// TMA cannot address them): the four epilogue warps load the stage with ordinary
+// loads, write the same 128-byte-swizzled layout TMA would produce (16-byte chunk c of
+// row r lands at chunk c ^ (r % 8) of its 1024-byte atom), make the generic-proxy
+// writes visible to the tensor core with fence.proxy.async, and arrive on the stage's
+// full barrier (128 arrivals instead of one transaction count).
+template <bool kTF32, int BN>
+__device__ __forceinline__ void lsu_stage(uint8_t* sa, uint8_t* sb, const GemmArgs& p, int b, int m0, int n0, int k0,
+                                          int t) {
+  using Elem = typename std::conditional<kTF32, uint32_t, uint16_t>::type;
+  constexpr int ES = sizeof(Elem), BK = 128 / ES, NATOM = 128 / ES;
+  const Elem* A = static_cast<const Elem*>(p.A) + static_cast<int64_t>(b) * p.sA;
+  const Elem* B = static_cast<const Elem*>(p.B) + static_cast<int64_t>(b) * p.sB;
+  for (int e = t; e < BM * BK; e += 128) {
+    const int row = e / BK, kc = e - row * BK;
+    const int gr = m0 + row, gk = k0 + kc;
+    const Elem v = (gr < p.m && gk < p.k) ? A[static_cast<int64_t>(gr) * p.lda + gk] : Elem(0);
+    const int byte = kc * ES;
+    *reinterpret_cast<Elem*>(sa + (row >> 3) * 1024 + (row & 7) * 128 + (((byte >> 4) ^ (row & 7)) << 4) +
+                             (byte & 15)) = v;
+  }
+  for (int e = t; e < BK * BN; e += 128) {
+    const int kr = e / BN, nc = e - kr * BN;
+    const int gk = k0 + kr, gn = n0 + nc;
+    const Elem v = (gk < p.k && gn < p.n) ? B[static_cast<int64_t>(gk) * p.ldb + gn] : Elem(0);
+    const int j = nc / NATOM, byte = (nc - j * NATOM) * ES;
+    const int off = kTF32 ? (kr * 128 + (((byte >> 5) ^ (kr & 3)) << 5) + (byte & 31))  // 128B_BASE32B
+                          : ((kr >> 3) * 1024 + (kr & 7) * 128 + (((byte >> 4) ^ (kr & 7)) << 4) + (byte & 15));
+    *reinterpret_cast<Elem*>(sb + j * (BK * 128) + off) = v;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <bool kTF32, int BN, int STAGES, bool kLsu>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, GemmArgs p,
                    int tiles_m, int a_batched, int b_batched) {
@@ -151,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kLsu ? 128 : 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
@@ -169,7 +214,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
+  if (kLsu && warp >= 2) {
+    // ---------------- LSU producer (unaligned operands) ----------------
+    const int t = threadIdx.x - 64;
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % STAGES;
+      if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+      uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
+      lsu_stage<kTF32, BN>(sa, sa + Cfg::A_BYTES, p, b, m0, n0, kt * Cfg::BK, t);
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+    }
+  }
+  if (!kLsu && warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
     const int za = a_batched ? b : 0, zb = b_batched ? b : 0;
     for (int kt = 0; kt < KT; ++kt) {
@@ -194,13 +250,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int kk = 0; kk < Cfg::BK / Cfg::UK; ++kk) {
         const uint64_t adesc = smem_desc(sa + kk * 32, 16, 1024);
-        const uint64_t bdesc = smem_desc(sb + kk * Cfg::UK * 128, Cfg::BK * 128, 1024);
+        const uint64_t bdesc = kTF32 ? smem_desc(sb + kk * Cfg::UK * 128, Cfg::BK * 128, 512, 1)
+                                     : smem_desc(sb + kk * Cfg::UK * 128, Cfg::BK * 128, 1024, 2);
         mma_issue<kTF32>(tmem_base, adesc, bdesc, Cfg::IDESC, (kt | kk) != 0);
       }
       mma_commit(&empty[s]);
     }
     mma_commit(tmem_full);
-  } else if (warp >= 2) {
+  }
+  if (warp >= 2) {
     // ---------------- epilogue: TMEM -> registers -> global ----------------
     const int quad = warp & 3;
     mbar_wait(tmem_full, 0);
@@ -276,19 +334,38 @@ const TcConfig* config_of(int family, int index) {
   return nullptr;
 }
 
+bool tma_ok(const GemmArgs& p, int es) {
+  auto aligned = [](const void* ptr, int bytes) { return (reinterpret_cast<uintptr_t>(ptr) % bytes) == 0; };
+  return aligned(p.A, 16) && aligned(p.B, 16) && (p.lda * es) % 16 == 0 && (p.ldb * es) % 16 == 0 &&
+         (p.batch == 1 || ((p.sA * es) % 16 == 0 && (p.sB * es) % 16 == 0));
+}
+
 template <bool kTF32, int BN, int STAGES>
 cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   using Cfg = TcCfg<kTF32, BN, STAGES>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<kTF32, BN, STAGES>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<kTF32, BN, STAGES, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(tc_gemm_kernel<kTF32, BN, STAGES, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  GemmArgs p = p0;
+  auto aligned = [](const void* ptr, int bytes) { return (reinterpret_cast<uintptr_t>(ptr) % bytes) == 0; };
+  p.c_vec = (p.ldc % 4 == 0) && (p.sC % 4 == 0) && aligned(p.C, 16);
+  const int tiles_m = (p.m + BM - 1) / BM, tiles_n = (p.n + BN - 1) / BN;
+  dim3 grid(tiles_m * tiles_n, p.batch);
+  if (!tma_ok(p, Cfg::ES)) {
+    CUtensorMap dummy;
+    std::memset(&dummy, 0, sizeof(dummy));
+    tc_gemm_kernel<kTF32, BN, STAGES, true><<<grid, kThreads, Cfg::SMEM_BYTES, s>>>(dummy, dummy, p, tiles_m, 0, 0);
+    return cudaGetLastError();
+  }
   EncodeFn enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
-  GemmArgs p = p0;
   const CUtensorMapDataType dt = kTF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const int a_batched = (p.batch > 1 && p.sA != 0), b_batched = (p.batch > 1 && p.sB != 0);
   CUtensorMap ma, mb;
@@ -314,15 +391,12 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
     cuuint32_t box[3] = {static_cast<cuuint32_t>(Cfg::NATOM), static_cast<cuuint32_t>(Cfg::BK), 1};
     cuuint32_t es[3] = {1, 1, 1};
     if (enc(&mb, dt, 3, const_cast<void*>(p.B), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            kTF32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  auto aligned = [](const void* ptr, int bytes) { return (reinterpret_cast<uintptr_t>(ptr) % bytes) == 0; };
-  p.c_vec = (p.ldc % 4 == 0) && (p.sC % 4 == 0) && aligned(p.C, 16);
-  const int tiles_m = (p.m + BM - 1) / BM, tiles_n = (p.n + BN - 1) / BN;
-  dim3 grid(tiles_m * tiles_n, p.batch);
-  tc_gemm_kernel<kTF32, BN, STAGES><<<grid, kThreads, Cfg::SMEM_BYTES, s>>>(ma, mb, p, tiles_m, a_batched, b_batched);
+  tc_gemm_kernel<kTF32, BN, STAGES, false><<<grid, kThreads, Cfg::SMEM_BYTES, s>>>(ma, mb, p, tiles_m, a_batched,
+                                                                                   b_batched);
   return cudaGetLastError();
 }
 
@@ -359,20 +433,10 @@ KernelChoice tc_family_choice(int family, int index) {
 const char* tc_last_reason() { return g_reason; }
 
 int tc_check(int family, int index, const GemmArgs& p) {
-  const TcConfig* c = config_of(family, index);
-  if (!c) {
+  (void)p;  // every shape runs: TMA when rows are 16-byte aligned, LSU staging otherwise
+  if (!config_of(family, index)) {
     snprintf(g_reason, sizeof(g_reason), "no tensor-core config %d in family %d", index, family);
     return KP_ENOENT;
-  }
-  const int es = c->tf32 ? 4 : 2;
-  auto aligned = [](const void* ptr, int bytes) { return (reinterpret_cast<uintptr_t>(ptr) % bytes) == 0; };
-  // TMA: 16-byte aligned base addresses and row / batch strides.
-  if (!aligned(p.A, 16) || !aligned(p.B, 16) || (p.lda * es) % 16 || (p.ldb * es) % 16 ||
-      (p.batch > 1 && ((p.sA * es) % 16 || (p.sB * es) % 16))) {
-    snprintf(g_reason, sizeof(g_reason),
-             "TMA needs 16-byte aligned operands and row strides (lda=%lld ldb=%lld, %d-byte elements)",
-             static_cast<long long>(p.lda), static_cast<long long>(p.ldb), es);
-    return KP_EINVAL;
   }
   return KP_OK;
 }

@@ -32,12 +32,27 @@ def _family_id(family: str | int) -> int:
         raise ValueError(f"unknown family {family!r}, expected one of {FAMILIES}") from None
 
 
+def family_list(spec: str | int) -> tuple:
+    """A table spec names one family ("simt") or several joined by '+' ("simt+tf32");
+    a combined table's columns are the families' config lists concatenated (their
+    5-tuples are disjoint)."""
+    if isinstance(spec, int):
+        return (spec,)
+    return tuple(spec.split("+"))
+
+
 @lru_cache(maxsize=None)
 def variant_id(config: KernelConfig, family: str | int = "simt") -> int:
-    """Kernel-library variant id of (family, config); KeyError if absent."""
+    """Kernel-library variant id of (family, config); for a combined spec the first
+    family holding the tuple wins.  KeyError if absent."""
     lib = _lib.load()
     choice = _lib.KernelChoice(*config.as_tuple())
-    return _lib.check(lib.kp_find_variant(_family_id(family), choice),
+    fams = family_list(family)
+    for fam in fams[:-1]:
+        rc = lib.kp_find_variant(_family_id(fam), choice)
+        if rc >= 0:
+            return rc
+    return _lib.check(lib.kp_find_variant(_family_id(fams[-1]), choice),
                       f"kp_find_variant({family}, {config.as_tuple()})")
 
 
@@ -52,16 +67,25 @@ def variant_info(vid: int) -> tuple[KernelConfig, str]:
 
 @lru_cache(maxsize=None)
 def family_configs(family: str | int) -> tuple[KernelConfig, ...]:
-    """The family's canonical config list (its benchmark-table column order)."""
+    """The family's canonical config list (its benchmark-table column order); for a
+    combined spec, the concatenation."""
     lib = _lib.load()
-    fid = _family_id(family)
-    size = _lib.check(lib.kp_family_size(fid), "kp_family_size")
-    return tuple(variant_info(_lib.check(lib.kp_family_variant(fid, i), "kp_family_variant"))[0]
-                 for i in range(size))
+    out = []
+    for fam in family_list(family):
+        fid = _family_id(fam)
+        size = _lib.check(lib.kp_family_size(fid), "kp_family_size")
+        out += [variant_info(_lib.check(lib.kp_family_variant(fid, i), "kp_family_variant"))[0]
+                for i in range(size)]
+    if len(set(out)) != len(out):
+        raise ValueError(f"families of {family!r} share config tuples")
+    return tuple(out)
 
 
 def input_dtype(family: str | int) -> torch.dtype:
-    return torch.bfloat16 if _family_id(family) == _lib.FAMILY_BF16 else torch.float32
+    dts = {torch.bfloat16 if _family_id(f) == _lib.FAMILY_BF16 else torch.float32 for f in family_list(family)}
+    if len(dts) != 1:
+        raise ValueError(f"families of {family!r} take different operand types; use separate tables")
+    return dts.pop()
 
 
 class GemmOperands:
