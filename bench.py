@@ -40,7 +40,7 @@ METRIC = "geomean % of oracle-best GFLOP/s (clustered set + tree); GFLOP/s vs FP
 def parse_args(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--batch", type=int, default=16, help="VGG16 images per step per GPU")
@@ -62,7 +62,7 @@ class ClockSampler:
                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, device_index: int, period: float = 0.1):
+    def __init__(self, device_index: int, period: float = 0.02):
         self.samples: list[int] = []
         self.reasons: set[str] = set()
         self.max_mhz = None
@@ -286,15 +286,23 @@ def run_ours(args, world, rank, local):
     ms_max = reduce_max(ms, world, device)
     value = step_flops * args.steps * world / (ms_max * 1e-3) / 1e9
 
-    # dominant launch: the layer with the largest summed device time
+    # dominant kernel: the (variant, problem) pair with the largest summed device time
+    # (conv4_2 and conv4_3 share one shape and variant, so they merge)
     layer_ms = [0.0] * len(bufs)
     for s in range(args.steps):
         for i, (a, b) in enumerate(per_launch[s]):
             layer_ms[i] += a.elapsed_time(b)
-    dom = max(range(len(bufs)), key=lambda i: layer_ms[i])
-    dname, dp, *_rest, dvid = bufs[dom]
-    dom_ms = layer_ms[dom] / args.steps
+    groups: dict = {}
+    for i, (name, p, _A, _W, _C, vid) in enumerate(bufs):
+        g = groups.setdefault((vid, p), {"ms": 0.0, "launches": 0, "names": []})
+        g["ms"] += layer_ms[i]
+        g["launches"] += args.steps
+        g["names"].append(name)
+    (dvid, dp), dg = max(groups.items(), key=lambda kv: kv[1]["ms"])
+    variant_ms = sum(g["ms"] for (v, _), g in groups.items() if v == dvid)
+    dom_ms = dg["ms"] / dg["launches"]
     dom_cfg, dom_fam = gemm.variant_info(dvid)
+    dname = "+".join(dg["names"])
     peak = gemm.ffma_peak_tflops(packed=True)
     achieved = dp.flops / (dom_ms * 1e-3) / 1e12
     traffic = None
@@ -306,6 +314,7 @@ def run_ours(args, world, rank, local):
                 traffic = rec.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    total_ms = sum(layer_ms)
 
     # e2e: host-pinned activations in, outputs out, through the dispatcher
     e2e = None
@@ -363,8 +372,10 @@ def run_ours(args, world, rank, local):
             "gpu_launches": len(bufs) * args.steps,
             "roofline": {"bound": "compute", "pipe": "fp32 FFMA2 (SIMT)", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes": 4 * (dp.m * dp.k + dp.k * dp.n + dp.m * dp.n),
+                         "flops_per_launch": dp.flops, "avg_launch_ms": dom_ms,
                          "kernel": f"{dom_fam}{dom_cfg.as_tuple()} on {dname} {[dp.m, dp.k, dp.n, dp.batch]}",
-                         "share_of_step": layer_ms[dom] / sum(layer_ms),
+                         "share_of_step": dg["ms"] / total_ms, "variant_share_of_step": variant_ms / total_ms,
                          "peak_source": "measured on this device by kp_ffma_peak (FFMA2 register loop); "
                                         "MEASURED_PEAKS.json has no FP32 SIMT figure"},
             "clocks": clocks.summary(),

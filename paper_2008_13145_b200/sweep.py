@@ -274,7 +274,9 @@ def _problem_set(name: str, batches) -> list[ProblemSize]:
 
     if name in shapes.NETWORKS:
         return shapes.network_problems(name, batches)
-    if name == "square":
+    if name == "square":  # 64..8192 squares + skinny extremes (full 640-config families)
+        return shapes.square_skinny_problems(sizes=(64, 128, 256, 512, 1024, 2048, 4096, 8192))
+    if name == "square16k":  # adds 16384^3 (tensor-core families)
         return shapes.square_skinny_problems()
     raise ValueError(f"unknown problem set {name!r}")
 
