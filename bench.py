@@ -49,6 +49,8 @@ def parse_args(argv=None):
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--method", default="kmeans")
     ap.add_argument("--classifier", default="treeA")
+    ap.add_argument("--workload", choices=("gemm-layers", "vgg16-infer"), default="gemm-layers",
+                    help="gemm-layers: BASELINE configs[1] (default); vgg16-infer: configs[2], data parallel")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args(argv)
@@ -388,12 +390,79 @@ def run_ours(args, world, rank, local):
     return 0
 
 
+def run_vgg16_infer(args, world, rank, local):
+    """BASELINE configs[2]: VGG16 inference, fp32, tree-dispatched GEMMs, data parallel
+    by batch (each rank its own images, replicated weights, no collective).  value =
+    images/s over all ranks; the forward is one CUDA graph per rank."""
+    import torch
+
+    from paper_2008_13145_b200.dispatch import Dispatcher
+    from paper_2008_13145_b200.vgg16 import Vgg16
+
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    pm, subset, tree, rep_test, rep_all, sel_t = train_selector(args.table, args.k, args.method, args.classifier)
+    disp = Dispatcher(tree, subset, pm.configs, args.family)
+    model = Vgg16(disp, args.batch, device, seed=0)
+    stream = torch.cuda.Stream(device)
+    g = torch.Generator().manual_seed(100 + rank)
+    host_x = torch.randn(args.batch, 224, 224, 3, generator=g).pin_memory()
+    host_y = torch.empty(args.batch, 1000, pin_memory=True)
+    model.input.copy_(host_x)
+    model.capture(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            model.forward(stream=stream)
+    torch.cuda.synchronize(device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                model.forward(stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+    barrier(world)
+    ms = reduce_max(e0.elapsed_time(e1), world, device)
+    flops = model.flops
+    value = args.batch * args.steps * world / (ms * 1e-3)
+    # e2e: images H2D from pinned memory, forward, logits D2H, every step
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    with torch.cuda.stream(stream):
+        f0.record(stream)
+        for _ in range(args.steps):
+            model.forward(host_x.to(device, non_blocking=True), stream=stream)
+            host_y.copy_(model.logits, non_blocking=True)
+        f1.record(stream)
+    torch.cuda.synchronize(device)
+    e2e_ms = reduce_max(f0.elapsed_time(f1), world, device)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (He-init weights)",
+                "config": {"workload": f"vgg16-infer-b{args.batch}-{args.method}{args.k}-{args.classifier}",
+                           "batch_per_gpu": args.batch, "family": args.family, "parallelism": f"dp{world}",
+                           "table": os.path.relpath(args.table, ROOT), "cuda_graph": True},
+                "gflops": flops * args.steps * world / (ms * 1e-3) / 1e9,
+                "selection": {"achieved_test": rep_test.achieved, "ceiling_test": rep_test.ceiling,
+                              "achieved_all_rows": rep_all.achieved},
+                "gpu_launches": (16 + 13 + 5) * args.steps, "clocks": clocks.summary(),
+                "e2e": {"value": args.batch * args.steps * world / (e2e_ms * 1e-3), "unit": "images/s",
+                        "h2d_bytes_per_step": host_x.numel() * 4, "d2h_bytes_per_step": host_y.numel() * 4}}
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def main(argv=None):
     args = parse_args(argv)
     world, rank, local = dist_setup(args)
     try:
         if args.impl == "reference":
             return run_reference(args, world, rank)
+        if args.workload == "vgg16-infer":
+            return run_vgg16_infer(args, world, rank, local)
         return run_ours(args, world, rank, local)
     finally:
         import torch.distributed as dist

@@ -13,7 +13,9 @@
 //   * tcgen05.commit frees each smem stage and finally signals the epilogue warps,
 //     which drain TMEM with tcgen05.ld (32x32b) and store fp32 rows.
 // Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA
-// issuer, warps 2..5 = epilogue (warp % 4 selects the TMEM lane quadrant).
+// issuer, warps 2..5 = epilogue (warp % 4 selects the TMEM lane quadrant).  The grid
+// is persistent (one CTA per SM) with two TMEM accumulators so each tile's epilogue
+// overlaps the next tile's MMAs.
 //
 // Config 5-tuple of these families (include/kpgemm.h KernelChoice), documented in
 // (tile_rows, tile_acc, tile_cols, wg_rows, wg_cols) =
@@ -131,8 +133,10 @@ struct TcCfg {
   static constexpr int A_BYTES = BM * 128;          // one stage of A (K-major)
   static constexpr int B_BYTES = BK * BN * ES;      // one stage of B (MN-major atoms)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  // two accumulators (double-buffered TMEM), power-of-two column allocation
+  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(2 * BN <= 512, "two accumulators must fit TMEM");
   static constexpr uint32_t IDESC = (1u << 4)                      // D = f32
                                     | ((kTF32 ? 2u : 1u) << 7)     // A = tf32 / bf16
                                     | ((kTF32 ? 2u : 1u) << 10)    // B = tf32 / bf16
@@ -176,33 +180,42 @@ __device__ __forceinline__ void lsu_stage(uint8_t* sa, uint8_t* sb, const GemmAr
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Persistent: gridDim.x = min(#tiles, #SMs) CTAs walk the tile list (m fastest, then
+// n, then batch) with stride gridDim.x.  The smem ring runs continuously across tiles
+// and TMEM holds two accumulators, so the epilogue of tile i overlaps the MMAs of
+// tile i+1 (tmem_full / tmem_empty mbarrier pairs).
 template <bool kTF32, int BN, int STAGES, bool kLsu>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, GemmArgs p,
-                   int tiles_m, int a_batched, int b_batched) {
+                   int tiles_m, int tiles_n, int a_batched, int b_batched) {
   using Cfg = TcCfg<kTF32, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + STAGES;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile_m = blockIdx.x % tiles_m, tile_n = blockIdx.x / tiles_m;
-  const int b = blockIdx.y;
-  const int m0 = tile_m * BM, n0 = tile_n * BN;
   const int KT = (p.k + Cfg::BK - 1) / Cfg::BK;
+  const int per_batch = tiles_m * tiles_n;
+  const int n_tiles = per_batch * p.batch;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], kLsu ? 128 : 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 4);  // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+    if (!kLsu) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -214,78 +227,98 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (kLsu && warp >= 2) {
-    // ---------------- LSU producer (unaligned operands) ----------------
-    const int t = threadIdx.x - 64;
-    for (int kt = 0; kt < KT; ++kt) {
-      const int s = kt % STAGES;
-      if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
-      uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
-      lsu_stage<kTF32, BN>(sa, sa + Cfg::A_BYTES, p, b, m0, n0, kt * Cfg::BK, t);
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
-    }
-  }
-  if (!kLsu && warp == 0 && lane == 0) {
+  if (warp == 0 && lane == 0 && !kLsu) {
     // ---------------- TMA producer ----------------
-    const int za = a_batched ? b : 0, zb = b_batched ? b : 0;
-    for (int kt = 0; kt < KT; ++kt) {
-      const int s = kt % STAGES;
-      if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
-      uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
-      uint8_t* sb = sa + Cfg::A_BYTES;
-      mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
-      tma_load_3d(sa, &mapA, &full[s], kt * Cfg::BK, m0, za);
+    int it = 0;  // global k-iteration counter (ring position across tiles)
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const int b = t / per_batch, r = t - b * per_batch;
+      const int m0 = (r % tiles_m) * BM, n0 = (r / tiles_m) * BN;
+      const int za = a_batched ? b : 0, zb = b_batched ? b : 0;
+      for (int kt = 0; kt < KT; ++kt, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);  // fresh barrier: passes
+        uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
+        uint8_t* sb = sa + Cfg::A_BYTES;
+        mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
+        tma_load_3d(sa, &mapA, &full[s], kt * Cfg::BK, m0, za);
 #pragma unroll
-      for (int j = 0; j < BN / Cfg::NATOM; ++j)
-        tma_load_3d(sb + j * (Cfg::BK * 128), &mapB, &full[s], n0 + j * Cfg::NATOM, kt * Cfg::BK, zb);
+        for (int j = 0; j < BN / Cfg::NATOM; ++j)
+          tma_load_3d(sb + j * (Cfg::BK * 128), &mapB, &full[s], n0 + j * Cfg::NATOM, kt * Cfg::BK, zb);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
-    for (int kt = 0; kt < KT; ++kt) {
-      const int s = kt % STAGES;
-      mbar_wait(&full[s], (kt / STAGES) & 1);
+    int it = 0, i = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+      const int a = i & 1;
+      mbar_wait(&tmem_empty[a], ((i >> 1) & 1) ^ 1);  // epilogue drained this accumulator
       tc_fence_after();
-      const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
-      const uint32_t sb = sa + Cfg::A_BYTES;
+      const uint32_t dtmem = tmem_base + a * BN;
+      for (int kt = 0; kt < KT; ++kt, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
+        const uint32_t sb = sa + Cfg::A_BYTES;
 #pragma unroll
-      for (int kk = 0; kk < Cfg::BK / Cfg::UK; ++kk) {
-        const uint64_t adesc = smem_desc(sa + kk * 32, 16, 1024);
-        const uint64_t bdesc = kTF32 ? smem_desc(sb + kk * Cfg::UK * 128, Cfg::BK * 128, 512, 1)
-                                     : smem_desc(sb + kk * Cfg::UK * 128, Cfg::BK * 128, 1024, 2);
-        mma_issue<kTF32>(tmem_base, adesc, bdesc, Cfg::IDESC, (kt | kk) != 0);
+        for (int kk = 0; kk < Cfg::BK / Cfg::UK; ++kk) {
+          const uint64_t adesc = smem_desc(sa + kk * 32, 16, 1024);
+          const uint64_t bdesc = kTF32 ? smem_desc(sb + kk * Cfg::UK * 128, Cfg::BK * 128, 512, 1)
+                                       : smem_desc(sb + kk * Cfg::UK * 128, Cfg::BK * 128, 1024, 2);
+          mma_issue<kTF32>(dtmem, adesc, bdesc, Cfg::IDESC, (kt | kk) != 0);
+        }
+        mma_commit(&empty[s]);
       }
-      mma_commit(&empty[s]);
+      mma_commit(&tmem_full[a]);
     }
-    mma_commit(tmem_full);
-  }
-  if (warp >= 2) {
-    // ---------------- epilogue: TMEM -> registers -> global ----------------
+  } else if (warp >= 2) {
+    // ---------------- epilogue (and LSU producer for unaligned operands) ----------------
     const int quad = warp & 3;
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    const int row = m0 + quad * 32 + lane;
-    float* out = static_cast<float*>(p.C) + static_cast<int64_t>(b) * p.sC + static_cast<int64_t>(row) * p.ldc;
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      float v[16];
-      tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + c, v);
-      if (row < p.m) {
-        const int col = n0 + c;
-        if (p.bias || p.relu) {
-#pragma unroll
-          for (int e = 0; e < 16; ++e)
-            if (col + e < p.n) v[e] = epilogue(p, v[e], col + e);
-        }
-        if (p.c_vec && col + 16 <= p.n) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<float4*>(out + col + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 16; ++e)
-            if (col + e < p.n) out[col + e] = v[e];
+    int it = 0, i = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+      const int b = t / per_batch, r = t - b * per_batch;
+      const int m0 = (r % tiles_m) * BM, n0 = (r / tiles_m) * BN;
+      if constexpr (kLsu) {
+        const int tid = threadIdx.x - 64;
+        for (int kt = 0; kt < KT; ++kt, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
+          lsu_stage<kTF32, BN>(sa, sa + Cfg::A_BYTES, p, b, m0, n0, kt * Cfg::BK, tid);
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
         }
       }
+      const int a = i & 1;
+      mbar_wait(&tmem_full[a], (i >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + quad * 32 + lane;
+      float* out = static_cast<float*>(p.C) + static_cast<int64_t>(b) * p.sC + static_cast<int64_t>(row) * p.ldc;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * BN + c, v);
+        if (row < p.m) {
+          const int col = n0 + c;
+          if (p.bias || p.relu) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (col + e < p.n) v[e] = epilogue(p, v[e], col + e);
+          }
+          if (p.c_vec && col + 16 <= p.n) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              *reinterpret_cast<float4*>(out + col + 4 * q) =
+                  make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (col + e < p.n) out[col + e] = v[e];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[a])) : "memory");
     }
   }
   tc_fence_before();
@@ -314,6 +347,17 @@ EncodeFn encode_fn() {
 }
 
 thread_local char g_reason[256] = "";
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
 
 struct TcConfig {
   bool tf32;
@@ -357,11 +401,14 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   auto aligned = [](const void* ptr, int bytes) { return (reinterpret_cast<uintptr_t>(ptr) % bytes) == 0; };
   p.c_vec = (p.ldc % 4 == 0) && (p.sC % 4 == 0) && aligned(p.C, 16);
   const int tiles_m = (p.m + BM - 1) / BM, tiles_n = (p.n + BN - 1) / BN;
-  dim3 grid(tiles_m * tiles_n, p.batch);
+  const int64_t n_tiles = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
+  if (n_tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  dim3 grid(static_cast<unsigned>(n_tiles < num_sms() ? n_tiles : num_sms()));
   if (!tma_ok(p, Cfg::ES)) {
     CUtensorMap dummy;
     std::memset(&dummy, 0, sizeof(dummy));
-    tc_gemm_kernel<kTF32, BN, STAGES, true><<<grid, kThreads, Cfg::SMEM_BYTES, s>>>(dummy, dummy, p, tiles_m, 0, 0);
+    tc_gemm_kernel<kTF32, BN, STAGES, true><<<grid, kThreads, Cfg::SMEM_BYTES, s>>>(dummy, dummy, p, tiles_m, tiles_n,
+                                                                                   0, 0);
     return cudaGetLastError();
   }
   EncodeFn enc = encode_fn();
@@ -395,8 +442,8 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  tc_gemm_kernel<kTF32, BN, STAGES, false><<<grid, kThreads, Cfg::SMEM_BYTES, s>>>(ma, mb, p, tiles_m, a_batched,
-                                                                                   b_batched);
+  tc_gemm_kernel<kTF32, BN, STAGES, false><<<grid, kThreads, Cfg::SMEM_BYTES, s>>>(ma, mb, p, tiles_m, tiles_n,
+                                                                                   a_batched, b_batched);
   return cudaGetLastError();
 }
 

@@ -47,7 +47,8 @@ def test_every_config_square(cuda_device, fam):
 
 @pytest.mark.parametrize("fam", ["bf16", "tf32"])
 @pytest.mark.parametrize("m,k,n,batch", [(1, 64, 64, 1), (130, 72, 200, 1), (1000, 576, 64, 2), (49, 4608, 512, 1),
-                                         (333, 1000, 1000, 1), (16, 8, 8, 3), (2048, 2048, 2048, 1)])
+                                         (333, 1000, 1000, 1), (16, 8, 8, 3), (2048, 2048, 2048, 1),
+                                         (4096, 512, 2048, 1), (1000, 256, 1000, 3)])
 def test_ragged_and_batched(cuda_device, fam, m, k, n, batch):
     for cfg in gemm.family_configs(fam)[::3]:
         _check(fam, cfg, m, k, n, batch, cuda_device, bcast=(batch > 1), seed=m + n)
