@@ -168,6 +168,29 @@ def train_selector(table_path: str, k: int, method: str, classifier: str):
     return pm, subset, tree, rep_test, rep_all, t
 
 
+def selection_grid(pm, ks=(4, 8), methods=("kmeans", "spectral", "pca_kmeans", "tree")):
+    """Held-out geomean fraction of oracle-best (evaluate.py:71-101) for other cells of
+    the paper's grid on the same table, treeA -- reported beside the headline cell."""
+    from paper_2008_13145_b200 import classify, dataset, evaluate, selection
+    from paper_2008_13145_b200.normalize import NormScheme, normalize
+
+    train, test = dataset.split(pm, dataset.SplitSpec(0.2, 0))
+    nm = normalize(train, NormScheme("scaled"))
+    feats = classify.problem_features(train.problems)
+    out = {}
+    for method in methods:
+        for k in ks:
+            try:
+                sub = selection.select_subset(method, nm, k, 0, problems=train.problems)
+            except Exception:
+                continue
+            labels = classify.label_best_in_subset(nm, sub)
+            tree = classify.train_tree(feats, labels, classify.TREE_PRESETS["A"], n_classes=sub.k_actual)
+            rep = evaluate.classifier_score(test, sub, lambda x, t=tree: classify.predict_tree(t, x))
+            out[f"{method}{k}"] = {"k_actual": sub.k_actual, "achieved_test": rep.achieved, "ceiling_test": rep.ceiling}
+    return out
+
+
 # ----------------------------------------------------------------- workload --
 def vgg16_layers(batch: int):
     from paper_2008_13145_b200 import shapes
@@ -371,6 +394,7 @@ def run_ours(args, world, rank, local):
                           "achieved_test": rep_test.achieved, "ceiling_test": rep_test.ceiling,
                           "achieved_all_rows": rep_all.achieved, "ceiling_all_rows": rep_all.ceiling,
                           "host_s": sel_t},
+            "selection_grid_treeA": selection_grid(pm),
             "gpu_launches": len(bufs) * args.steps,
             "roofline": {"bound": "compute", "pipe": "fp32 FFMA2 (SIMT)", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,

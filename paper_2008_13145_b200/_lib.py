@@ -91,7 +91,8 @@ def load(path: str | os.PathLike | None = None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path is not None else LIB_PATH
+        # KPGEMM_LIB: development override (e.g. an experimental build); default in-tree
+        p = Path(path) if path is not None else Path(os.environ.get("KPGEMM_LIB", LIB_PATH))
         if not p.exists():
             raise KernelLibraryError(
                 f"{p} not found: build it with `make -C paper_2008_13145_b200/csrc -j8` "

@@ -180,8 +180,25 @@ __device__ __forceinline__ void lsu_stage(uint8_t* sa, uint8_t* sb, const GemmAr
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// Persistent: gridDim.x = min(#tiles, #SMs) CTAs walk the tile list (m fastest, then
-// n, then batch) with stride gridDim.x.  The smem ring runs continuously across tiles
+// Tile order inside one batch: bands of kGroupM m-tiles; within a band n-major with m
+// fastest, so the ~148 tiles in flight share a few A panels and a few B panels in L2
+// (plain m-fastest order streams all of A once per n column).
+constexpr int kGroupM = 16;
+template <int BN>
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& b, int& m0, int& n0) {
+  const int per_batch = tiles_m * tiles_n;
+  b = t / per_batch;
+  const int r = t - b * per_batch;
+  const int band = r / (kGroupM * tiles_n);
+  const int first = band * kGroupM;
+  const int rows = tiles_m - first < kGroupM ? tiles_m - first : kGroupM;
+  const int local = r - band * kGroupM * tiles_n;
+  m0 = (first + local % rows) * BM;
+  n0 = (local / rows) * BN;
+}
+
+// Persistent: gridDim.x = min(#tiles, #SMs) CTAs walk the tile list (tile_coords
+// order, then batch) with stride gridDim.x.  The smem ring runs continuously across tiles
 // and TMEM holds two accumulators, so the epilogue of tile i overlaps the MMAs of
 // tile i+1 (tmem_full / tmem_empty mbarrier pairs).
 template <bool kTF32, int BN, int STAGES, bool kLsu>
@@ -231,8 +248,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- TMA producer ----------------
     int it = 0;  // global k-iteration counter (ring position across tiles)
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const int b = t / per_batch, r = t - b * per_batch;
-      const int m0 = (r % tiles_m) * BM, n0 = (r / tiles_m) * BN;
+      int b, m0, n0;
+      tile_coords<BN>(t, tiles_m, tiles_n, b, m0, n0);
       const int za = a_batched ? b : 0, zb = b_batched ? b : 0;
       for (int kt = 0; kt < KT; ++kt, ++it) {
         const int s = it % STAGES;
@@ -276,8 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;
     int it = 0, i = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-      const int b = t / per_batch, r = t - b * per_batch;
-      const int m0 = (r % tiles_m) * BM, n0 = (r / tiles_m) * BN;
+      int b, m0, n0;
+      tile_coords<BN>(t, tiles_m, tiles_n, b, m0, n0);
       if constexpr (kLsu) {
         const int tid = threadIdx.x - 64;
         for (int kt = 0; kt < KT; ++kt, ++it) {
