@@ -73,6 +73,16 @@ struct F1Cfg {
   static constexpr int WTC = f1_pick_wtc(R, C, WGR, WGC);
   static constexpr int WTR = 32 / WTC;
   static constexpr int WPC = WGC / WTC;  // warps across the work-group columns
+  // Shared-memory wavefronts (measured): an LDS.64/128 costs half
+  // when each pair of adjacent lanes reads the same address.  Only one operand can be
+  // pair-shared in an outer-product warp tile, so pair the lanes on the operand with
+  // more floats per thread per k-step: the LHS (R floats, if read as >= 2-wide vectors)
+  // or the RHS (C floats, if VC >= 2).
+  static constexpr int COST_PAIR_A = (A >= 2 && WTC >= 2 ? R : 2 * R) + 2 * C;  // in half-wavefronts
+  static constexpr int COST_PAIR_B = 2 * R + (VC >= 2 && WTR >= 2 ? C : 2 * C);
+  // Measured: only worth it for LDS.128 RHS fragments (VC == 4); with 8-byte RHS reads
+  // the row-fastest lane order costs more in the epilogue than it saves.
+  static constexpr bool PAIR_B = VC == 4 && COST_PAIR_B < COST_PAIR_A;
   static constexpr bool B_CHUNKS = (BN % 4) == 0;
   static_assert(WTC > 0, "work group not tileable by warps");
   static_assert(NT % 32 == 0, "work group must be whole warps");
@@ -89,8 +99,11 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int ty = (warp / Cfg::WPC) * Cfg::WTR + lane / Cfg::WTC;
-  const int tx = (warp % Cfg::WPC) * Cfg::WTC + lane % Cfg::WTC;
+  // lane -> (row, col) inside the warp tile: adjacent lanes share the paired operand
+  const int lr = Cfg::PAIR_B ? lane % Cfg::WTR : lane / Cfg::WTC;
+  const int lc = Cfg::PAIR_B ? lane / Cfg::WTR : lane % Cfg::WTC;
+  const int ty = (warp / Cfg::WPC) * Cfg::WTR + lr;
+  const int tx = (warp % Cfg::WPC) * Cfg::WTC + lc;
 
   const int64_t gm = blockIdx.x / groups_n;
   const int gn = blockIdx.x - static_cast<int>(gm * groups_n);
