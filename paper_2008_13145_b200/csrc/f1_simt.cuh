@@ -61,9 +61,15 @@ struct F1Cfg {
   static constexpr int MIN_BLOCKS = (KP_F1_WARPS * 32 / NT) > 1 ? (KP_F1_WARPS * 32 / NT) : 1;
   static constexpr int kBudget = (227 * 1024) / (MIN_BLOCKS < 4 ? MIN_BLOCKS : 4) - 1024;
   static constexpr int stage_floats(int bk) { return BM * (bk + PADA) + bk * BN; }
-  static constexpr int BK = (2 * 4 * stage_floats(32) <= kBudget)   ? 32
-                            : (2 * 4 * stage_floats(16) <= kBudget) ? 16
-                                                                    : 8;
+#ifndef KP_F1_ZIGZAG
+#define KP_F1_ZIGZAG 0
+#endif
+#ifndef KP_F1_MAX_BK
+#define KP_F1_MAX_BK 32
+#endif
+  static constexpr int BK = (KP_F1_MAX_BK >= 32 && 2 * 4 * stage_floats(32) <= kBudget)   ? 32
+                            : (KP_F1_MAX_BK >= 16 && 2 * 4 * stage_floats(16) <= kBudget) ? 16
+                                                                                        : 8;
   static constexpr int SA = BK + PADA;  // LHS smem row stride (floats)
   static constexpr int SB = BN;         // RHS smem row stride (floats)
   static constexpr int STAGE = stage_floats(BK);
@@ -252,11 +258,16 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
 #pragma unroll
           for (int r = 0; r < R; ++r) acc[r][0].x = __fmaf_rn(a[r][i], w[0], acc[r][0].x);
         } else {
+          // Zig-zag order: consecutive FFMA2s share the scalar a[r] (same row) or, at a
+          // row change, the RHS pair -- one operand comes from the reuse cache, so the
+          // other two fit the register-file ports at full FFMA2 rate.
 #pragma unroll
           for (int r = 0; r < R; ++r)
 #pragma unroll
-            for (int c = 0; c < CP; ++c)
+            for (int cc = 0; cc < CP; ++cc) {
+              const int c = (KP_F1_ZIGZAG && (r & 1)) ? CP - 1 - cc : cc;
               acc[r][c] = __ffma2_rn(make_float2(a[r][i], a[r][i]), make_float2(w[2 * c], w[2 * c + 1]), acc[r][c]);
+            }
         }
       }
     }

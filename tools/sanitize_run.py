@@ -1,0 +1,37 @@
+"""Small launches of every family / code path for compute-sanitizer (memcheck, racecheck,
+synccheck): F0 and F1 vector + scalar (unaligned) paths, tcgen05 TMA and LSU paths,
+epilogue bias/ReLU, im2col and max-pool."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2008_13145_b200 import _lib, gemm  # noqa: E402
+from paper_2008_13145_b200.dataset import KernelConfig  # noqa: E402
+
+dev = torch.device("cuda")
+cases = [("paper", KernelConfig(4, 4, 4, 16, 16)), ("paper", KernelConfig(1, 8, 2, 8, 8)),
+         ("simt", KernelConfig(8, 4, 8, 16, 16)), ("simt", KernelConfig(4, 8, 8, 16, 8)),
+         ("simt", KernelConfig(2, 1, 1, 128, 1)), ("simt", KernelConfig(1, 2, 8, 1, 128))]
+cases += [(f, c) for f in ("bf16", "tf32") for c in gemm.family_configs(f)[:2]]
+for fam, cfg in cases:
+    dt = gemm.input_dtype(fam)
+    for (m, k, n) in ((70, 64, 72), (33, 27, 45)):  # aligned / unaligned rows
+        A = torch.rand(m, k, device=dev).to(dt)
+        B = torch.rand(k, n, device=dev).to(dt)
+        gemm.matmul(A, B, cfg, fam)
+lib = _lib.load()
+A = torch.rand(70, 64, device=dev)
+W = torch.rand(64, 72, device=dev)
+C = torch.empty(70, 72, device=dev)
+bias = torch.rand(72, device=dev)
+vid = gemm.variant_id(KernelConfig(8, 4, 8, 16, 16), "simt")
+_lib.check(lib.kp_gemm_ex(vid, 70, 64, 72, 1, A.data_ptr(), 64, 0, W.data_ptr(), 72, 0, C.data_ptr(), 72, 0,
+                          bias.data_ptr(), 1, None), "gemm_ex")
+x = torch.rand(2, 6, 6, 5, device=dev)
+cols = torch.empty(2 * 36, 45, device=dev)
+_lib.check(lib.kp_im2col3x3_nhwc(x.data_ptr(), 2, 6, 6, 5, cols.data_ptr(), 45, None), "im2col")
+y = torch.empty(2, 3, 3, 5, device=dev)
+_lib.check(lib.kp_maxpool2x2_nhwc(x.data_ptr(), 2, 6, 6, 5, y.data_ptr(), None), "pool")
+torch.cuda.synchronize()
+print("sanitize run ok")
