@@ -52,18 +52,12 @@ struct F1Cfg {
   // Occupancy target: >= 16 resident warps per SM (4 per scheduler) so FFMA2 issue
   // hides LDS latency.  MIN_BLOCKS feeds __launch_bounds__ (caps registers at
   // 65536 / (MIN_BLOCKS * NT)) and the per-CTA shared-memory budget.
-#ifndef KP_F1_ILP
-#define KP_F1_ILP 0
-#endif
 #ifndef KP_F1_WARPS
 #define KP_F1_WARPS 16
 #endif
   static constexpr int MIN_BLOCKS = (KP_F1_WARPS * 32 / NT) > 1 ? (KP_F1_WARPS * 32 / NT) : 1;
   static constexpr int kBudget = (227 * 1024) / (MIN_BLOCKS < 4 ? MIN_BLOCKS : 4) - 1024;
   static constexpr int stage_floats(int bk) { return BM * (bk + PADA) + bk * BN; }
-#ifndef KP_F1_ZIGZAG
-#define KP_F1_ZIGZAG 0
-#endif
 #ifndef KP_F1_MAX_BK
 #define KP_F1_MAX_BK 32
 #endif
@@ -211,39 +205,6 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
     }
     const float* as = smem + (kt % STAGES) * Cfg::STAGE;
     const float* bs = as + BM * SA;
-#if KP_F1_ILP
-    // Register double buffering: the LHS block for k..k+A-1 and the RHS row for k+1
-    // are read from shared memory while the FFMA2s of step k issue.
-    float a[2][R][A];
-    float w[2][C];
-    auto load_a = [&](float(&dst)[R][A], int kk) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) lds_vec<A>(as + (r * WGR + ty) * SA + kk, dst[r]);
-    };
-    auto load_w = [&](float(&dst)[C], int k) {
-#pragma unroll
-      for (int cv = 0; cv < C / VC; ++cv) lds_vec<VC>(bs + k * SB + cv * WGC * VC + tx * VC, dst + cv * VC);
-    };
-    load_a(a[0], 0);
-    load_w(w[0], 0);
-#pragma unroll
-    for (int k = 0; k < BK; ++k) {
-      const int j = k / A, i = k % A;
-      if (i == 0 && k + A < BK) load_a(a[(j + 1) & 1], k + A);
-      if (k + 1 < BK) load_w(w[(k + 1) & 1], k + 1);
-      if constexpr (C == 1) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) acc[r][0].x = __fmaf_rn(a[j & 1][r][i], w[k & 1][0], acc[r][0].x);
-      } else {
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-#pragma unroll
-          for (int c = 0; c < CP; ++c)
-            acc[r][c] = __ffma2_rn(make_float2(a[j & 1][r][i], a[j & 1][r][i]),
-                                   make_float2(w[k & 1][2 * c], w[k & 1][2 * c + 1]), acc[r][c]);
-      }
-    }
-#else
 #pragma unroll
     for (int kk = 0; kk < BK; kk += A) {
       float a[R][A];
@@ -258,20 +219,14 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
 #pragma unroll
           for (int r = 0; r < R; ++r) acc[r][0].x = __fmaf_rn(a[r][i], w[0], acc[r][0].x);
         } else {
-          // Zig-zag order: consecutive FFMA2s share the scalar a[r] (same row) or, at a
-          // row change, the RHS pair -- one operand comes from the reuse cache, so the
-          // other two fit the register-file ports at full FFMA2 rate.
 #pragma unroll
           for (int r = 0; r < R; ++r)
 #pragma unroll
-            for (int cc = 0; cc < CP; ++cc) {
-              const int c = (KP_F1_ZIGZAG && (r & 1)) ? CP - 1 - cc : cc;
+            for (int c = 0; c < CP; ++c)
               acc[r][c] = __ffma2_rn(make_float2(a[r][i], a[r][i]), make_float2(w[2 * c], w[2 * c + 1]), acc[r][c]);
-            }
         }
       }
     }
-#endif
   }
   cp_async_wait<0>();
 

@@ -3,11 +3,6 @@
 // dataset.py:19-31) so the 640 kernels build in parallel.
 #include "families.h"
 #include "f1_simt.cuh"
-#include "f1v2_simt.cuh"
-
-#ifndef KP_F1_V2
-#define KP_F1_V2 0
-#endif
 
 #ifndef KP_WG_INDEX
 #error "compile with -DKP_WG_INDEX=<0..9>"
@@ -25,10 +20,7 @@ constexpr int WGC = kWgPairs[KP_WG_INDEX][1];
 template <int RI, int AI, int CI>
 void put(GemmLaunchFn* table) {
   const int cfg = ((RI * 4 + AI) * 4 + CI) * kNumWgPairs + KP_WG_INDEX;
-  if constexpr (KP_F1_V2)
-    table[cfg] = &f1v2_launch<(1 << RI), (1 << AI), (1 << CI), WGR, WGC>;
-  else
-    table[cfg] = &f1_launch<(1 << RI), (1 << AI), (1 << CI), WGR, WGC>;
+  table[cfg] = &f1_launch<(1 << RI), (1 << AI), (1 << CI), WGR, WGC>;
 }
 
 template <int RI, int AI>
