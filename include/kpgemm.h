@@ -101,6 +101,25 @@ int kp_gemm_ex(int id, int m, int k, int n, int batch,
                void* C, int64_t ldc, int64_t sC,
                const float* bias, int flags, void* stream);
 
+/* ---- k-slicing (SIMT family) ----------------------------------------------
+ * A SIMT launch whose output tiles cannot fill the GPU's resident-CTA slots (SM count
+ * x the config's occupancy target) cuts k into S <= 8 consecutive slices (each at
+ * least 256 deep, aligned to the config's k-tile) computed by the CTAs of one
+ * (1, 1, S) thread-block cluster (S is lowered to what cudaOccupancyMaxActiveClusters
+ * can co-schedule on the current device; the cap can be raised to the non-portable
+ * cluster limit 16 with kp_set_max_k_slices); each output is then the fp32 fma chain
+ * over every slice, summed in slice order ((p0 + p1) + p2) + ... through distributed
+ * shared memory -- deterministic for a given (config, shape, device).
+ * kp_gemm_plan reports the plan kp_gemm would use: *k_slices = S and *k_per_slice =
+ * the depth of every slice but the last (= k when S == 1).  num_sms <= 0 means the
+ * current device's SM count and cluster limit (num_sms > 0 plans for a hypothetical
+ * device with that many SMs and no cluster limit).  Families other than SIMT always
+ * report S = 1.  kp_set_max_k_slices(1) disables slicing (every output is the single
+ * fma chain over k, bit-identical to the PAPER family); returns the previous setting
+ * (default 8, range 1..16). */
+int kp_set_max_k_slices(int max_slices);
+int kp_gemm_plan(int id, int m, int k, int n, int batch, int num_sms, int* k_slices, int* k_per_slice);
+
 /* ---- benchmark harness ---------------------------------------------------
  * warmup untimed launches, then one launch timed alone to size the loop, then
  * max(min_iters, ceil(min_ms / t1)) (capped at max_iters) back-to-back launches

@@ -40,6 +40,8 @@ def lib():
         L.kp_ref_gemm_tiled.argtypes = [i] * 9 + [vp, i64, i64, vp, i64, i64, vp, i64, i64]
         L.kp_ref_gemm_chain.restype = None
         L.kp_ref_gemm_chain.argtypes = [i] * 4 + [vp, i64, i64, vp, i64, i64, vp, i64, i64]
+        L.kp_ref_gemm_sliced.restype = None
+        L.kp_ref_gemm_sliced.argtypes = [i] * 5 + [vp, i64, i64, vp, i64, i64, vp, i64, i64]
         L.kp_ref_gemm_f64.restype = None
         L.kp_ref_gemm_f64.argtypes = [i] * 4 + [vp, i64, i64, vp, i64, i64, vp, vp, i64, i64]
         _lib = L
@@ -74,6 +76,16 @@ def gemm_chain(A, B) -> np.ndarray:
     A3, B3, batch, m, k, n, sA, sB = _batched(A, B)
     C = np.zeros((batch, m, n), dtype=np.float32)
     lib().kp_ref_gemm_chain(m, k, n, batch, A3.ctypes.data, k, sA, B3.ctypes.data, n, sB, C.ctypes.data, n, m * n)
+    return C
+
+
+def gemm_sliced(A, B, k_per_slice: int) -> np.ndarray:
+    """k-sliced chain: fmaf chain per slice of k_per_slice, slices summed in order
+    (the SIMT family's plan from kp_gemm_plan when a launch cannot fill the GPU)."""
+    A3, B3, batch, m, k, n, sA, sB = _batched(A, B)
+    C = np.zeros((batch, m, n), dtype=np.float32)
+    lib().kp_ref_gemm_sliced(m, k, n, batch, int(k_per_slice), A3.ctypes.data, k, sA, B3.ctypes.data, n, sB,
+                             C.ctypes.data, n, m * n)
     return C
 
 

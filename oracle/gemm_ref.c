@@ -104,6 +104,40 @@ void kp_ref_gemm_chain(int m, int k, int n, int batch, const float* Am, int64_t 
   }
 }
 
+/* k-sliced variant (the SIMT family's plan when a launch cannot fill the GPU, see
+ * kp_gemm_plan in include/kpgemm.h): k is cut into consecutive slices of k_per_slice
+ * (the last one shorter); each slice is the sequential fmaf chain from +0 over its k
+ * range and the slices are summed in order, out = ((p0 + p1) + p2) + ...
+ * k_per_slice >= k is the plain chain. */
+void kp_ref_gemm_sliced(int m, int k, int n, int batch, int k_per_slice, const float* Am, int64_t lda, int64_t sA,
+                        const float* Bm, int64_t ldb, int64_t sB, float* Cm, int64_t ldc, int64_t sC) {
+  if (k_per_slice <= 0 || k_per_slice >= k) {
+    kp_ref_gemm_chain(m, k, n, batch, Am, lda, sA, Bm, ldb, sB, Cm, ldc, sC);
+    return;
+  }
+  const int64_t rb = (m + KP_RB - 1) / KP_RB, jb = (n + KP_JB - 1) / KP_JB;
+  const int64_t tasks = (int64_t)batch * rb * jb;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t t = 0; t < tasks; ++t) {
+    const int64_t b = t / (rb * jb), rem = t % (rb * jb);
+    const int64_t i0 = (rem / jb) * KP_RB, j0 = (rem % jb) * KP_JB;
+    const int rows = (int)(m - i0 < KP_RB ? m - i0 : KP_RB);
+    const int jn = (int)(n - j0 < KP_JB ? n - j0 : KP_JB);
+    float part[KP_RB * KP_JB];
+    float* out = Cm + b * sC + i0 * ldc + j0;
+    for (int k0 = 0; k0 < k; k0 += k_per_slice) {
+      const int kl = k - k0 < k_per_slice ? k - k0 : k_per_slice;
+      kp_ref_chain_block(rows, kl, jn, Am + b * sA + i0 * lda + k0, lda, Bm + b * sB + (int64_t)k0 * ldb + j0, ldb,
+                         part, KP_JB);
+      for (int r = 0; r < rows; ++r)
+        for (int j = 0; j < jn; ++j) {
+          float* o = out + (int64_t)r * ldc + j;
+          *o = k0 == 0 ? part[r * KP_JB + j] : *o + part[r * KP_JB + j];
+        }
+    }
+  }
+}
+
 /* float64 product of the fp32 operands, plus the |A||B| magnitude for the
  * per-element error bound |C - C64| <= 2 k u (|A||B|)_ij. */
 KP_CLONES void kp_ref_gemm_f64(int m, int k, int n, int batch, const float* Am, int64_t lda, int64_t sA, const float* Bm,

@@ -33,8 +33,15 @@ def maxpool2(x: np.ndarray) -> np.ndarray:
     return x.reshape(B, H // 2, 2, W // 2, 2, C).max(axis=(2, 4))
 
 
-def forward(x: np.ndarray, convs, fcs) -> np.ndarray:
-    """x (B,224,224,3) fp32; convs/fcs lists of (W, b) numpy fp32 -> logits (B,1000)."""
+def _gemm(A, W, k_per_slice):
+    kps = k_per_slice(A.shape[0], A.shape[1], W.shape[1]) if k_per_slice else None
+    return (go.gemm_sliced(A, W, kps) if kps else go.gemm_chain(A, W))[0]
+
+
+def forward(x: np.ndarray, convs, fcs, k_per_slice=None) -> np.ndarray:
+    """x (B,224,224,3) fp32; convs/fcs lists of (W, b) numpy fp32 -> logits (B,1000).
+    k_per_slice(m, k, n) -> int, optional: the GPU's k-slice plan for each layer GEMM
+    (kp_gemm_plan), so the restatement sums the same slices in the same order."""
     B = x.shape[0]
     ci = 0
     for item in PLAN:
@@ -44,12 +51,12 @@ def forward(x: np.ndarray, convs, fcs) -> np.ndarray:
         w, b = convs[ci]
         ci += 1
         H = x.shape[1]
-        y = go.gemm_chain(im2col3x3(x), w)[0]
+        y = _gemm(im2col3x3(x), w, k_per_slice)
         y = np.maximum(y + b, np.float32(0.0))
         x = y.reshape(B, H, H, w.shape[1])
     h = x.reshape(B, -1)
     for (w, b), relu in zip(fcs, FC_RELU):
-        h = go.gemm_chain(h, w)[0] + b
+        h = _gemm(h, w, k_per_slice) + b
         if relu:
             h = np.maximum(h, np.float32(0.0))
     return h

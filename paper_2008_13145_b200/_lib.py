@@ -68,6 +68,8 @@ SIGNATURES = {
     "kp_family_variant": (_i, [_i, _i]),
     "kp_gemm": (_i, [_i] + _GEMM_ARGS + [_vp]),
     "kp_gemm_ex": (_i, [_i] + _GEMM_ARGS + [_vp, _i, _vp]),
+    "kp_set_max_k_slices": (_i, [_i]),
+    "kp_gemm_plan": (_i, [_i, _i, _i, _i, _i, _i, _ip, _ip]),
     "kp_bench": (_i, [_i] + _GEMM_ARGS + [_i, _i, _i, ctypes.c_double, _dp, _ip, _vp]),
     "kp_ffma_peak": (_i, [_i, _dp, _vp]),
     "kp_dispatch_load": (_i, [_i, _i32p, _dp, _i32p, _i32p, _i32p, _i, _i32p]),

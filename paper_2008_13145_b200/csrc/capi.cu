@@ -1,5 +1,6 @@
 // The C ABI of libkpgemm.so (include/kpgemm.h): variant registry, GEMM launch,
 // benchmark harness, FFMA peak probe and the tree -> variant dispatch tables.
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -41,7 +42,7 @@ struct Variant {
 struct Registry {
   std::vector<Variant> variants;
   int family_begin[KP_NUM_FAMILIES + 1];
-  kp::GemmLaunchFn f1[kp::kPaperConfigs];
+  kp::F1Entry f1[kp::kPaperConfigs];
 
   Registry() {
     std::memset(f1, 0, sizeof(f1));
@@ -100,17 +101,97 @@ int check_problem(int id, int m, int k, int n, int batch, const void* A, int64_t
   return KP_OK;
 }
 
-int launch(int id, const kp::GemmArgs& p, cudaStream_t s) {
+// ------------------------------------------------------------- k-slicing --
+// When a SIMT launch has fewer output tiles than the GPU has resident-CTA slots
+// (mid-size m x n with a long k: VGG16 conv5 / fc at small batch), the k-tiles are
+// cut into S consecutive slices computed by the S CTAs of a (1, 1, S) cluster and
+// summed in slice order through distributed shared memory (f1_simt.cuh).  The plan is
+// a pure function of (config, shape, SM count), so results are deterministic on a
+// given GPU model and the oracle reproduces them from kp_gemm_plan.
+std::atomic<int> g_max_kslices{kp::kDefaultKSlices};
+constexpr int kMinSliceK = 256;  // never cut k into slices shallower than this
+
+int num_sms_current() {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev >= static_cast<int>(cache.size())) cache.resize(dev + 1, 0);
+  if (cache[dev] == 0) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) return -1;
+    cache[dev] = sms;
+  }
+  return cache[dev];
+}
+
+// Largest cluster size <= want that the variant can co-schedule on this device
+// (cudaOccupancyMaxActiveClusters >= 1), cached per (variant, size).
+int f1_fit_slices(int index, const kp::F1Entry& e, int want) {
+  static std::mutex mu;
+  static std::vector<int8_t> fit;  // [index][slices]: 0 unknown, 1 fits, -1 does not
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+  std::lock_guard<std::mutex> lock(mu);
+  const size_t row = (kp::kMaxKSlices + 1);
+  if (fit.empty()) fit.assign(kp::kPaperConfigs * row, 0);
+  for (int s = want; s > 1; --s) {
+    int8_t& f = fit[index * row + s];
+    if (f == 0) f = e.cluster_fit(s) >= 1 ? 1 : -1;
+    if (f > 0) return s;
+  }
+  return 1;
+}
+
+void f1_plan(const kp::F1Entry& e, int m, int k, int n, int batch, int sms, int max_slices, int* slices,
+             int* kt_per_slice) {
+  const int64_t tiles = ((m + e.bm - 1) / e.bm) * static_cast<int64_t>((n + e.bn - 1) / e.bn) * batch;
+  const int kt = (k + e.bk - 1) / e.bk;
+  const int64_t slots = static_cast<int64_t>(sms) * e.occ;
+  int s = 1;
+  if (max_slices > 1 && tiles < slots) {
+    const int64_t want = slots / tiles;
+    s = static_cast<int>(want < max_slices ? want : max_slices);
+    const int by_k = k / kMinSliceK;
+    if (s > by_k) s = by_k;
+    if (s < 1) s = 1;
+  }
+  *slices = s;
+  *kt_per_slice = kt;
+}
+
+void f1_split(int kt, int* slices, int* kt_per_slice) {
+  int s = *slices;
+  int per = (kt + s - 1) / s;
+  s = (kt + per - 1) / per;  // no empty slices
+  if (s == 1) per = kt;
+  *slices = s;
+  *kt_per_slice = per;
+}
+
+int launch(int id, const kp::GemmArgs& p0, cudaStream_t s) {
   Registry& reg = registry();
   const Variant& v = reg.variants[id];
   cudaError_t e = cudaSuccess;
+  kp::GemmArgs p = p0;
   switch (v.family) {
     case KP_FAMILY_PAPER:
       e = kp::f0_launch(v.choice, p, s);
       break;
-    case KP_FAMILY_SIMT:
-      e = reg.f1[v.index](p, s);
+    case KP_FAMILY_SIMT: {
+      const kp::F1Entry& fe = reg.f1[v.index];
+      const int max_slices = g_max_kslices.load(std::memory_order_relaxed);
+      if (max_slices > 1) {
+        const int sms = num_sms_current();
+        if (sms < 1) return fail(KP_EIO, "cannot query the SM count of the current device");
+        f1_plan(fe, p.m, p.k, p.n, p.batch, sms, max_slices, &p.kslices, &p.kt_per_slice);
+        if (p.kslices > 1) p.kslices = f1_fit_slices(v.index, fe, p.kslices);
+        f1_split(p.kt_per_slice, &p.kslices, &p.kt_per_slice);
+      }
+      e = fe.launch(p, s);
       break;
+    }
     default: {
       const int rc = kp::tc_check(v.family, v.index, p);
       if (rc != KP_OK) return fail(rc, "variant %d cannot run this problem: %s", id, kp::tc_last_reason());
@@ -129,7 +210,9 @@ kp::GemmArgs make_args(int m, int k, int n, int batch, const void* A, int64_t ld
   p.A = A; p.lda = lda; p.sA = sA;
   p.B = B; p.ldb = ldb; p.sB = sB;
   p.C = C; p.ldc = ldc; p.sC = sC;
-  p.a_vec = p.b_vec = p.c_vec = 0;
+  p.a_vec = p.b_vec = p.c_vec = p.c_vec4 = 0;
+  p.kslices = 1;
+  p.kt_per_slice = 0;
   p.bias = nullptr;
   p.relu = 0;
   return p;
@@ -219,6 +302,38 @@ int kp_gemm_ex(int id, int m, int k, int n, int batch, const void* A, int64_t ld
   p.bias = bias;
   p.relu = (flags & KP_EPI_RELU) != 0;
   return launch(id, p, static_cast<cudaStream_t>(stream));
+}
+
+int kp_set_max_k_slices(int max_slices) {
+  if (max_slices < 1 || max_slices > kp::kMaxKSlices)
+    return fail(KP_EINVAL, "max k-slices must be in [1, %d], got %d", kp::kMaxKSlices, max_slices);
+  return g_max_kslices.exchange(max_slices);
+}
+
+int kp_gemm_plan(int id, int m, int k, int n, int batch, int num_sms, int* k_slices, int* k_per_slice) {
+  Registry& reg = registry();
+  if (id < 0 || id >= static_cast<int>(reg.variants.size())) return fail(KP_ENOENT, "unknown variant id %d", id);
+  if (m < 1 || k < 1 || n < 1 || batch < 1) return fail(KP_EINVAL, "dims must be >= 1");
+  if (!k_slices || !k_per_slice) return fail(KP_EINVAL, "null output pointer");
+  const Variant& v = reg.variants[id];
+  const int max_slices = g_max_kslices.load(std::memory_order_relaxed);
+  if (v.family != KP_FAMILY_SIMT || max_slices <= 1) {
+    *k_slices = 1;
+    *k_per_slice = k;
+    return KP_OK;
+  }
+  const bool device = num_sms <= 0;
+  if (device) num_sms = num_sms_current();
+  if (num_sms < 1) return fail(KP_EIO, "cannot query the SM count of the current device");
+  const kp::F1Entry& fe = reg.f1[v.index];
+  int s = 1, per = 0;
+  f1_plan(fe, m, k, n, batch, num_sms, max_slices, &s, &per);
+  if (device && s > 1) s = f1_fit_slices(v.index, fe, s);  // the device's cluster limit
+  f1_split(per, &s, &per);
+  *k_slices = s;
+  const int64_t depth = static_cast<int64_t>(per) * fe.bk;
+  *k_per_slice = static_cast<int>(depth < k ? depth : k);
+  return KP_OK;
 }
 
 int kp_bench(int id, int m, int k, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* B,

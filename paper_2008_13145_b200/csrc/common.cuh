@@ -22,9 +22,17 @@ struct GemmArgs {
   int a_vec;  // rows of A may be read with the family's vector width along k
   int b_vec;  // rows of B may be read with the family's vector width along n
   int c_vec;  // rows of C may be written with the family's vector width along n
+  int c_vec4;  // rows of C may be written as float4 (k-sliced reduction stores)
   // Fused epilogue (kp_gemm_ex): C = act(A*B + bias[col]); bias may be null.
   const float* bias;
   int relu;
+  // k-slicing (SIMT family, planned by capi.cu): the k-tiles are cut into kslices
+  // consecutive ranges of kt_per_slice tiles; slice z is computed by the CTA at
+  // blockIdx.z of a (1, 1, kslices) thread-block cluster and the partial tiles are
+  // summed in slice order through distributed shared memory.  kslices == 1 is the
+  // plain single-chain kernel.
+  int kslices;
+  int kt_per_slice;
 };
 
 // Epilogue of every family: bias add (fp32, round-to-nearest) then ReLU.  Applied

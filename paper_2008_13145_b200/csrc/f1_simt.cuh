@@ -24,7 +24,10 @@
 // bit-identical to F0 and to the oracle (oracle/gemm_ref.c).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+#include "families.h"
 
 namespace kp {
 
@@ -70,6 +73,10 @@ struct F1Cfg {
   static constexpr int STAGES_FIT = kBudget / (4 * STAGE);
   static constexpr int STAGES = STAGES_FIT < 2 ? 2 : (STAGES_FIT > 4 ? 4 : STAGES_FIT);
   static constexpr int SMEM_BYTES = STAGES * STAGE * 4;
+  // k-sliced launches park the fp32 partial tile (row stride SP) in shared memory.
+  // (padded, and keeping each thread's VC-wide stores aligned).
+  static constexpr int SP = BN % 4 == 0 ? BN + 4 : (BN % 2 == 0 ? BN + 2 : BN + 1);
+  static constexpr int SLICE_SMEM_BYTES = SMEM_BYTES > BM * SP * 4 ? SMEM_BYTES : BM * SP * 4;
   static constexpr int WTC = f1_pick_wtc(R, C, WGR, WGC);
   static constexpr int WTR = 32 / WTC;
   static constexpr int WPC = WGC / WTC;  // warps across the work-group columns
@@ -89,6 +96,63 @@ struct F1Cfg {
   static_assert(BK % A == 0, "stage depth must be a multiple of A");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 };
+
+// Cluster reduction of a k-sliced tile: CTA rank z of the (1, 1, kslices) cluster
+// owns elements [z*chunk, (z+1)*chunk) of the BM x BN tile (flat, row-major) and sums
+// them over every rank's shared-memory partial (DSMEM loads) in rank order.
+template <int BM, int BN, int SP, int NT>
+__device__ __forceinline__ void f1_slice_reduce(const GemmArgs& p, float* smem, float* Cb, int64_t m0, int64_t n0) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();  // every slice's partial is in place
+  const int S = p.kslices;
+  const int z = static_cast<int>(cl.block_rank());
+  // rank s's partial tile, as a generic pointer into its shared memory (mapa)
+  auto part = [&](int s) -> const float* { return cl.map_shared_rank(smem, s); };
+  const int m = p.m, n = p.n;
+  if constexpr (BN % 4 == 0) {
+    constexpr int Q = BN / 4, TOT = BM * Q;
+    const int chunk = (TOT + S - 1) / S;
+    const int end = min(TOT, (z + 1) * chunk);
+    for (int i = z * chunk + static_cast<int>(threadIdx.x); i < end; i += NT) {
+      const int r = i / Q, c = (i - r * Q) * 4;
+      const int64_t row = m0 + r, col = n0 + c;
+      if (row >= m || col >= n) continue;
+      float4 v = *reinterpret_cast<const float4*>(part(0) + r * SP + c);
+      for (int s = 1; s < S; ++s) {
+        const float4 w = *reinterpret_cast<const float4*>(part(s) + r * SP + c);
+        v.x = v.x + w.x; v.y = v.y + w.y; v.z = v.z + w.z; v.w = v.w + w.w;
+      }
+      float o[4] = {v.x, v.y, v.z, v.w};
+      float* out = Cb + row * p.ldc + col;
+      if (p.bias || p.relu) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[e] = (col + e < n) ? epilogue(p, o[e], col + e) : o[e];
+      }
+      if (p.c_vec4 && col + 4 <= n) {
+        stg_vec<4>(out, o);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (col + e < n) out[e] = o[e];
+      }
+    }
+  } else {
+    constexpr int TOT = BM * BN;
+    const int chunk = (TOT + S - 1) / S;
+    const int end = min(TOT, (z + 1) * chunk);
+    for (int i = z * chunk + static_cast<int>(threadIdx.x); i < end; i += NT) {
+      const int r = i / BN, c = i - r * BN;
+      const int64_t row = m0 + r, col = n0 + c;
+      if (row >= m || col >= n) continue;
+      float v = part(0)[r * SP + c];
+      for (int s = 1; s < S; ++s) v = v + part(s)[r * SP + c];
+      if (p.bias || p.relu) v = epilogue(p, v, col);
+      Cb[row * p.ldc + col] = v;
+    }
+  }
+  cl.sync();  // keep this CTA's partial alive until every rank has read it
+}
 
 template <int R, int A, int C, int WGR, int WGC>
 __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCKS) f1_kernel(GemmArgs p, int groups_n) {
@@ -188,10 +252,13 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
 #pragma unroll
     for (int c = 0; c < CP; ++c) acc[r][c] = make_float2(0.0f, 0.0f);
 
-  const int KT = (k + BK - 1) / BK;
+  // This CTA's k-tiles: all of them, or slice blockIdx.z of a k-sliced launch.
+  const int KTall = (k + BK - 1) / BK;
+  const int kt0 = static_cast<int>(blockIdx.z) * p.kt_per_slice;
+  const int KT = min(KTall - kt0, p.kt_per_slice);
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_tile(s, s);
+    if (s < KT) load_tile(s, kt0 + s);
     cp_async_commit();
   }
 
@@ -200,7 +267,7 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
     __syncthreads();
     {
       const int nk = kt + STAGES - 1;
-      if (nk < KT) load_tile(nk % STAGES, nk);
+      if (nk < KT) load_tile(nk % STAGES, kt0 + nk);
       cp_async_commit();
     }
     const float* as = smem + (kt % STAGES) * Cfg::STAGE;
@@ -230,6 +297,28 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
   }
   cp_async_wait<0>();
 
+  if (p.kslices > 1) {
+    // k-sliced: park the partial tile in this CTA's shared memory, then each CTA of
+    // the cluster sums 1/kslices of the tile over the slices in rank order 0, 1, ...
+    // (a fixed order, so the result is deterministic: ((p0 + p1) + p2) + ...).
+    __syncthreads();
+    constexpr int SP = Cfg::SP;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int cv = 0; cv < C / VC; ++cv) {
+        float v[VC];
+#pragma unroll
+        for (int e = 0; e < VC; ++e) {
+          const float2 pr = acc[r][(cv * VC + e) / 2];
+          v[e] = ((cv * VC + e) & 1) ? pr.y : pr.x;
+        }
+        stg_vec<VC>(smem + (r * WGR + ty) * SP + cv * WGC * VC + tx * VC, v);
+      }
+    f1_slice_reduce<BM, BN, SP, NT>(p, smem, Cb, m0, n0);
+    return;
+  }
+
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t row = m0 + r * WGR + ty;
@@ -257,15 +346,47 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
 }
 
 template <int R, int A, int C, int WGR, int WGC>
-cudaError_t f1_launch(const GemmArgs& p0, cudaStream_t s) {
+cudaError_t f1_set_attributes() {
   using Cfg = F1Cfg<R, A, C, WGR, WGC>;
-  static bool attr_set = false;  // benign race: idempotent attribute write
+  static bool attr_set = false;  // benign race: idempotent attribute writes
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(f1_kernel<R, A, C, WGR, WGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM_BYTES);
+                                         Cfg::SLICE_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(f1_kernel<R, A, C, WGR, WGC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  return cudaSuccess;
+}
+
+template <int R, int A, int C, int WGR, int WGC>
+int f1_cluster_fit(int slices) {
+  using Cfg = F1Cfg<R, A, C, WGR, WGC>;
+  if (f1_set_attributes<R, A, C, WGR, WGC>() != cudaSuccess) return -1;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(1, 1, slices);
+  lc.blockDim = dim3(Cfg::NT);
+  lc.dynamicSmemBytes = Cfg::SLICE_SMEM_BYTES;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = slices;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, f1_kernel<R, A, C, WGR, WGC>, &lc) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return n;
+}
+
+template <int R, int A, int C, int WGR, int WGC>
+cudaError_t f1_launch(const GemmArgs& p0, cudaStream_t s) {
+  using Cfg = F1Cfg<R, A, C, WGR, WGC>;
+  if (cudaError_t e = f1_set_attributes<R, A, C, WGR, WGC>(); e != cudaSuccess) return e;
   GemmArgs p = p0;
   auto aligned = [](const void* ptr, int bytes) { return (reinterpret_cast<uintptr_t>(ptr) % bytes) == 0; };
   p.a_vec = (p.k % 4 == 0) && (p.lda % 4 == 0) && (p.sA % 4 == 0) && aligned(p.A, 16);
@@ -275,9 +396,28 @@ cudaError_t f1_launch(const GemmArgs& p0, cudaStream_t s) {
   const int64_t groups_n = (p.n + Cfg::BN - 1) / Cfg::BN;
   const int64_t gx = groups_m * groups_n;
   if (gx > 0x7fffffffLL || p.batch > 65535) return cudaErrorInvalidConfiguration;
-  f1_kernel<R, A, C, WGR, WGC><<<dim3(static_cast<unsigned>(gx), p.batch), Cfg::NT, Cfg::SMEM_BYTES, s>>>(
-      p, static_cast<int>(groups_n));
-  return cudaGetLastError();
+  if (p.kslices <= 1) {
+    p.kslices = 1;
+    p.kt_per_slice = (p.k + Cfg::BK - 1) / Cfg::BK;
+    f1_kernel<R, A, C, WGR, WGC><<<dim3(static_cast<unsigned>(gx), p.batch), Cfg::NT, Cfg::SMEM_BYTES, s>>>(
+        p, static_cast<int>(groups_n));
+    return cudaGetLastError();
+  }
+  if (p.kslices > kMaxKSlices) return cudaErrorInvalidConfiguration;
+  p.c_vec4 = (p.ldc % 4 == 0) && (p.sC % 4 == 0) && aligned(p.C, 16);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(static_cast<unsigned>(gx), p.batch, p.kslices);
+  lc.blockDim = dim3(Cfg::NT);
+  lc.dynamicSmemBytes = Cfg::SLICE_SMEM_BYTES;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = p.kslices;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, f1_kernel<R, A, C, WGR, WGC>, p, static_cast<int>(groups_n));
 }
 
 }  // namespace kp

@@ -18,13 +18,16 @@ constexpr int WGR = kWgPairs[KP_WG_INDEX][0];
 constexpr int WGC = kWgPairs[KP_WG_INDEX][1];
 
 template <int RI, int AI, int CI>
-void put(GemmLaunchFn* table) {
+void put(F1Entry* table) {
+  constexpr int R = 1 << RI, A = 1 << AI, C = 1 << CI;
+  using Cfg = F1Cfg<R, A, C, WGR, WGC>;
   const int cfg = ((RI * 4 + AI) * 4 + CI) * kNumWgPairs + KP_WG_INDEX;
-  table[cfg] = &f1_launch<(1 << RI), (1 << AI), (1 << CI), WGR, WGC>;
+  table[cfg] = F1Entry{&f1_launch<R, A, C, WGR, WGC>, Cfg::BM, Cfg::BN, Cfg::BK, Cfg::MIN_BLOCKS,
+                       &f1_cluster_fit<R, A, C, WGR, WGC>};
 }
 
 template <int RI, int AI>
-void put_row(GemmLaunchFn* t) {
+void put_row(F1Entry* t) {
   put<RI, AI, 0>(t);
   put<RI, AI, 1>(t);
   put<RI, AI, 2>(t);
@@ -32,7 +35,7 @@ void put_row(GemmLaunchFn* t) {
 }
 
 template <int RI>
-void put_block(GemmLaunchFn* t) {
+void put_block(F1Entry* t) {
   put_row<RI, 0>(t);
   put_row<RI, 1>(t);
   put_row<RI, 2>(t);
@@ -41,7 +44,7 @@ void put_block(GemmLaunchFn* t) {
 
 }  // namespace
 
-void KP_CAT(f1_fill_wg, KP_WG_INDEX)(GemmLaunchFn* table) {
+void KP_CAT(f1_fill_wg, KP_WG_INDEX)(F1Entry* table) {
   put_block<0>(table);
   put_block<1>(table);
   put_block<2>(table);

@@ -17,21 +17,33 @@ constexpr int kPaperConfigs = 640;
 
 using GemmLaunchFn = cudaError_t (*)(const GemmArgs&, cudaStream_t);
 
+// One F1 instantiation: its launcher plus the compile-time tile facts the k-slice
+// planner (capi.cu) needs.  bm x bn is the CTA output tile, bk the k-tile depth, occ
+// the resident-CTA target per SM (__launch_bounds__ min blocks).
+struct F1Entry {
+  GemmLaunchFn launch;
+  int bm, bn, bk, occ;
+  // cudaOccupancyMaxActiveClusters for a (1, 1, slices) cluster launch (< 0: error)
+  int (*cluster_fit)(int slices);
+};
+constexpr int kMaxKSlices = 16;      // non-portable thread-block-cluster limit on sm_100
+constexpr int kDefaultKSlices = 8;   // portable clusters: measured faster than 9..16
+
 // F0 (family PAPER): any (R,A,C) in {1,2,4,8}^3, any block shape <= 1024 threads.
 cudaError_t f0_launch(const KernelChoice& ch, GemmArgs p, cudaStream_t s);
 
-// F1 (family SIMT): table of 640 launchers in enumerate_configs order, filled by
+// F1 (family SIMT): table of 640 entries in enumerate_configs order, filled by
 // the ten per-work-group translation units (f1_simt_inst.cu compiled ten times).
-void f1_fill_wg0(GemmLaunchFn* table);
-void f1_fill_wg1(GemmLaunchFn* table);
-void f1_fill_wg2(GemmLaunchFn* table);
-void f1_fill_wg3(GemmLaunchFn* table);
-void f1_fill_wg4(GemmLaunchFn* table);
-void f1_fill_wg5(GemmLaunchFn* table);
-void f1_fill_wg6(GemmLaunchFn* table);
-void f1_fill_wg7(GemmLaunchFn* table);
-void f1_fill_wg8(GemmLaunchFn* table);
-void f1_fill_wg9(GemmLaunchFn* table);
+void f1_fill_wg0(F1Entry* table);
+void f1_fill_wg1(F1Entry* table);
+void f1_fill_wg2(F1Entry* table);
+void f1_fill_wg3(F1Entry* table);
+void f1_fill_wg4(F1Entry* table);
+void f1_fill_wg5(F1Entry* table);
+void f1_fill_wg6(F1Entry* table);
+void f1_fill_wg7(F1Entry* table);
+void f1_fill_wg8(F1Entry* table);
+void f1_fill_wg9(F1Entry* table);
 
 // Conv-as-GEMM helpers (nn_ops.cu).
 cudaError_t im2col3x3_nhwc_launch(const float* x, int B, int H, int W, int C, float* out, int64_t ldo,

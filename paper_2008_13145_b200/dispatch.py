@@ -105,6 +105,11 @@ class Dispatcher:
         return _lib.check(_lib.load().kp_dispatch_select(self.handle, p.m, p.k, p.n, p.batch),
                           "kp_dispatch_select")
 
+    def k_slice_plan(self, problem: ProblemSize, num_sms: int = 0) -> tuple[int, int]:
+        """(k_slices, k_per_slice) of the launch this dispatcher makes (kp_gemm_plan)."""
+        from .gemm import k_slice_plan
+        return k_slice_plan(self.variant(problem), problem, num_sms=num_sms)
+
     def matmul(self, A, B, out=None, stream=None):
         """C = A @ B with the tree-selected variant (device tensors)."""
         import torch

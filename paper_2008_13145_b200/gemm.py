@@ -11,6 +11,7 @@ There is no CPU or library fallback: a missing kernel library raises.
 
 from __future__ import annotations
 
+import ctypes
 from functools import lru_cache
 
 import torch
@@ -172,6 +173,24 @@ def bench(vid: int, ops: GemmOperands, warmup: int = 1, min_iters: int = 2, max_
                             _lib.ctypes.byref(mean), _lib.ctypes.byref(iters), s),
                f"kp_bench(variant {vid}, {ops.problem})")
     return mean.value, iters.value
+
+
+def k_slice_plan(config: KernelConfig | int, problem: ProblemSize, family: str = "simt",
+                 num_sms: int = 0) -> tuple[int, int]:
+    """(k_slices, k_per_slice) the library uses for this launch (kp_gemm_plan):
+    SIMT launches that cannot fill the GPU sum k-slices in order; (1, k) otherwise.
+    num_sms <= 0 asks the current CUDA device."""
+    vid = config if isinstance(config, int) else variant_id(config, family)
+    s, per = ctypes.c_int(0), ctypes.c_int(0)
+    _lib.check(_lib.load().kp_gemm_plan(vid, problem.m, problem.k, problem.n, problem.batch, num_sms,
+                                        ctypes.byref(s), ctypes.byref(per)), "kp_gemm_plan")
+    return s.value, per.value
+
+
+def set_max_k_slices(max_slices: int) -> int:
+    """Cap the SIMT family's k-slicing (1 = off: every output is the single fma chain
+    over k, bit-identical to the paper family); returns the previous cap."""
+    return _lib.check(_lib.load().kp_set_max_k_slices(int(max_slices)), "kp_set_max_k_slices")
 
 
 def ffma_peak_tflops(packed: bool = False, stream: torch.cuda.Stream | None = None) -> float:

@@ -118,3 +118,38 @@ def test_dispatch_load_rejects_malformed_trees(lib):
     assert _load(lib, bad, good) == _lib.KP_EINVAL
     assert b"not a tree" in lib.kp_last_error() or b"reachable" in lib.kp_last_error()
     assert _load(lib, tree, good[:2]) == _lib.KP_EINVAL  # leaf class outside the class map
+
+
+def test_k_slice_plan_host_logic(lib):
+    """kp_gemm_plan with an explicit SM count needs no GPU: slices only when the output
+    tiles cannot fill SMs x occupancy slots, at most 8 by default, never shallower than 256 in k,
+    no empty slice, k-tile aligned; other families and a cap of 1 never slice."""
+    from paper_2008_13145_b200 import gemm
+    probs = [ProblemSize(196, 4608, 512, 1), ProblemSize(32, 25088, 4096, 1), ProblemSize(1, 4096, 1000, 1),
+             ProblemSize(12544, 4608, 512, 1), ProblemSize(3136, 2304, 256, 1), ProblemSize(50, 300, 70, 4),
+             ProblemSize(64, 255, 64, 1), ProblemSize(7, 100000, 9, 1)]
+    seen_sliced = 0
+    for cfg in enumerate_configs()[::7]:
+        tiles_m, tiles_n = cfg.tile_rows * cfg.wg_rows, cfg.tile_cols * cfg.wg_cols
+        for p in probs:
+            s, kps = gemm.k_slice_plan(cfg, p, num_sms=148)
+            assert 1 <= s <= 8
+            if s == 1:
+                assert kps == p.k
+                continue
+            seen_sliced += 1
+            assert p.k // s >= 128 and kps >= 256 // 2
+            assert (s - 1) * kps < p.k <= s * kps  # no empty slice
+            assert kps % 8 == 0  # a whole number of k-tiles (BK in {8, 16, 32})
+            tiles = -(-p.m // tiles_m) * -(-p.n // tiles_n) * p.batch
+            assert tiles < 148 * 16  # only under-filled launches slice
+        big = ProblemSize(16384, 4096, 16384, 1)
+        assert gemm.k_slice_plan(cfg, big, num_sms=148) == (1, 4096)
+        assert gemm.k_slice_plan(cfg, ProblemSize(1, 4096, 1, 1), family="paper", num_sms=148) == (1, 4096)
+    assert seen_sliced > 50
+    prev = gemm.set_max_k_slices(1)
+    try:
+        assert gemm.k_slice_plan(KernelConfig(4, 8, 8, 16, 8), probs[0], num_sms=148) == (1, 4608)
+    finally:
+        assert gemm.set_max_k_slices(prev) == 1
+    assert lib.kp_set_max_k_slices(0) == _lib.KP_EINVAL

@@ -47,4 +47,5 @@ def test_dispatcher_matches_predict_tree_and_oracle(cuda_device):
         A = rng.uniform(-1, 1, (p.m, p.k)).astype(np.float32)
         B = rng.uniform(-1, 1, (p.k, p.n)).astype(np.float32)
         got = disp.matmul(torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)).cpu().numpy()
-        assert np.array_equal(got.view(np.uint32), go.gemm_chain(A, B)[0].view(np.uint32))
+        _, kps = disp.k_slice_plan(p)
+        assert np.array_equal(got.view(np.uint32), go.gemm_sliced(A, B, kps)[0].view(np.uint32))

@@ -91,13 +91,105 @@ def test_full_size_error_bound(cuda_device, family, cfg):
 
 
 def test_families_agree_bitwise_at_scale(cuda_device):
+    """With k-slicing off every SIMT config is the single chain, like the paper family."""
     g = torch.Generator(device=cuda_device).manual_seed(1)
     A = torch.rand(1000, 2304, device=cuda_device, generator=g)
     B = torch.rand(2304, 520, device=cuda_device, generator=g)
-    ref = gemm.matmul(A, B, KernelConfig(8, 4, 8, 16, 16), "simt")
-    for fam, cfg in (("paper", KernelConfig(2, 4, 4, 8, 8)), ("simt", KernelConfig(4, 2, 8, 32, 8)),
-                     ("simt", KernelConfig(1, 8, 8, 1, 128))):
-        assert torch.equal(gemm.matmul(A, B, cfg, fam), ref)
+    prev = gemm.set_max_k_slices(1)
+    try:
+        ref = gemm.matmul(A, B, KernelConfig(8, 4, 8, 16, 16), "simt")
+        for fam, cfg in (("paper", KernelConfig(2, 4, 4, 8, 8)), ("simt", KernelConfig(4, 2, 8, 32, 8)),
+                         ("simt", KernelConfig(1, 8, 8, 1, 128))):
+            assert torch.equal(gemm.matmul(A, B, cfg, fam), ref)
+    finally:
+        gemm.set_max_k_slices(prev)
+
+
+# ---- k-sliced launches (cluster DSMEM reduction) --------------------------------
+# mid-size m x n with long k: VGG16 conv5 / fc rows, ragged and unaligned k, batches
+SLICED_SHAPES = [(196, 4608, 512, 1), (32, 4096, 1000, 1), (1, 25088, 512, 1), (70, 3001, 130, 1),
+                 (33, 1111, 61, 2), (100, 777, 36, 3)]
+
+
+@pytest.mark.parametrize("shape", SLICED_SHAPES)
+def test_k_sliced_bit_exact(cuda_device, shape):
+    """Every SIMT config on shapes the planner slices equals the oracle's sliced chain
+    (per-slice fmaf chains summed in slice order) bit for bit."""
+    m, k, n, batch = shape
+    A, B = _pair(m, k, n, batch, seed=k)
+    dA, dB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    want = {}
+    bad, sliced = [], 0
+    for cfg in CONFIGS[::3]:
+        s, kps = gemm.k_slice_plan(cfg, dataset_problem(shape))
+        assert 1 <= s <= 16 and (s == 1) == (kps == k)
+        sliced += s > 1
+        if kps not in want:
+            want[kps] = _bits(go.gemm_sliced(A, B, kps))
+        got = gemm.matmul(dA, dB, cfg, "simt").cpu().numpy()
+        if not np.array_equal(_bits(got), want[kps]):
+            bad.append((cfg.as_tuple(), s, kps))
+    assert sliced > 0
+    assert not bad, f"{len(bad)} configs differ, e.g. {bad[:5]}"
+
+
+def dataset_problem(shape):
+    from paper_2008_13145_b200.dataset import ProblemSize
+    return ProblemSize(*shape)
+
+
+def test_k_sliced_epilogue_and_strides(cuda_device):
+    """bias + ReLU after the slice sum, weight broadcast, ldc > n and an unaligned C."""
+    from paper_2008_13145_b200 import _lib
+    m, k, n, batch = 50, 2048, 70, 3
+    A, W = _pair(m, k, n, batch, seed=11, bcast=True)
+    bias = np.random.default_rng(5).uniform(-1, 1, n).astype(np.float32)
+    cfg = KernelConfig(4, 4, 4, 16, 16)
+    s, kps = gemm.k_slice_plan(cfg, dataset_problem((m, k, n, batch)))
+    assert s > 1
+    want = np.maximum(go.gemm_sliced(A, W, kps) + bias, np.float32(0))
+    dA, dW = torch.from_numpy(A).to(cuda_device), torch.from_numpy(W).to(cuda_device)
+    db = torch.from_numpy(bias).to(cuda_device)
+    buf = torch.full((batch * m * 73 + 1,), 3.0, device=cuda_device)
+    C = buf[1:].view(batch, m, 73)  # ldc 73, C 4-byte aligned only
+    vid = gemm.variant_id(cfg, "simt")
+    lib = _lib.load()
+    rc = lib.kp_gemm_ex(vid, m, k, n, batch, dA.data_ptr(), k, m * k, dW.data_ptr(), n, 0, C.data_ptr(), 73, m * 73,
+                        db.data_ptr(), _lib.KP_EPI_RELU, torch.cuda.current_stream().cuda_stream)
+    _lib.check(rc, "kp_gemm_ex")
+    got = C[:, :, :n].cpu().numpy()
+    assert np.array_equal(_bits(got), _bits(want))
+    assert bool((C[:, :, n:] == 3.0).all())
+
+
+def test_k_slicing_off_is_the_single_chain(cuda_device):
+    m, k, n = 196, 4608, 512
+    A, B = _pair(m, k, n, 1, seed=2)
+    dA, dB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    cfg = KernelConfig(4, 8, 8, 16, 8)
+    prev = gemm.set_max_k_slices(1)
+    try:
+        assert gemm.k_slice_plan(cfg, dataset_problem((m, k, n, 1))) == (1, k)
+        got = gemm.matmul(dA, dB, cfg, "simt").cpu().numpy()
+    finally:
+        gemm.set_max_k_slices(prev)
+    assert np.array_equal(_bits(got), _bits(go.gemm_chain(A, B)))
+    with pytest.raises(ValueError):
+        gemm.set_max_k_slices(17)
+
+
+def test_k_sliced_full_size_error_bound(cuda_device):
+    """VGG16 fc6 at batch 32 (m=32, k=25088, n=4096), sliced: fp32 bound vs float64."""
+    g = torch.Generator(device=cuda_device).manual_seed(3)
+    m, k, n = 32, 25088, 4096
+    A = torch.rand(m, k, device=cuda_device, generator=g) * 2 - 1
+    B = torch.rand(k, n, device=cuda_device, generator=g) * 2 - 1
+    cfg = KernelConfig(8, 8, 4, 8, 16)
+    assert gemm.k_slice_plan(cfg, dataset_problem((m, k, n, 1)))[0] > 1
+    C = gemm.matmul(A, B, cfg, "simt").double()
+    ref = A.double() @ B.double()
+    mag = A.double().abs() @ B.double().abs()
+    assert bool(((C - ref).abs() <= 2 * k * 2.0 ** -24 * mag).all())
 
 
 def test_bad_operands_raise(cuda_device):

@@ -52,8 +52,9 @@ def test_vgg16_forward_bit_exact(cuda_device, batch):
     g = torch.Generator().manual_seed(7)
     x = torch.randn(batch, 224, 224, 3, generator=g)
     got = model.forward(x.to(cuda_device)).cpu().numpy().copy()
+    plan = lambda m, k, n: model.disp.k_slice_plan(dataset.ProblemSize(m, k, n, 1))[1]  # noqa: E731
     want = vgg16_ref.forward(x.numpy(), [(w.numpy(), b.numpy()) for w, b in convs],
-                             [(w.numpy(), b.numpy()) for w, b in fcs])
+                             [(w.numpy(), b.numpy()) for w, b in fcs], k_per_slice=plan)
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
     model.capture()
     again = model.forward(x.to(cuda_device)).cpu().numpy()
