@@ -101,9 +101,10 @@ int kp_gemm_ex(int id, int m, int k, int n, int batch,
                void* C, int64_t ldc, int64_t sC,
                const float* bias, int flags, void* stream);
 
-/* ---- k-slicing (SIMT family) ----------------------------------------------
- * A SIMT launch whose output tiles cannot fill the GPU's resident-CTA slots (SM count
- * x the config's occupancy target) cuts k into S <= 8 consecutive slices (each at
+/* ---- k-slicing (SIMT, TF32 and BF16 families) ----------------------------
+ * A launch whose output tiles cannot fill the GPU's resident-CTA slots (SIMT: SM count
+ * x the config's occupancy target; tensor-core families: at most half the SMs get a
+ * tile) cuts k into S <= 8 consecutive slices (each at
  * least 256 deep, aligned to the config's k-tile) computed by the CTAs of one
  * (1, 1, S) thread-block cluster (S is lowered to what cudaOccupancyMaxActiveClusters
  * can co-schedule on the current device; the cap can be raised to the non-portable
@@ -113,9 +114,10 @@ int kp_gemm_ex(int id, int m, int k, int n, int batch,
  * kp_gemm_plan reports the plan kp_gemm would use: *k_slices = S and *k_per_slice =
  * the depth of every slice but the last (= k when S == 1).  num_sms <= 0 means the
  * current device's SM count and cluster limit (num_sms > 0 plans for a hypothetical
- * device with that many SMs and no cluster limit).  Families other than SIMT always
- * report S = 1.  kp_set_max_k_slices(1) disables slicing (every output is the single
- * fma chain over k, bit-identical to the PAPER family); returns the previous setting
+ * device with that many SMs and no cluster limit).  The PAPER family keeps the paper's
+ * geometry and always reports S = 1.  kp_set_max_k_slices(1) disables slicing (every
+ * SIMT output is then the single fma chain over k, bit-identical to the PAPER family,
+ * and the tensor-core families run persistent); returns the previous setting
  * (default 8, range 1..16). */
 int kp_set_max_k_slices(int max_slices);
 int kp_gemm_plan(int id, int m, int k, int n, int batch, int num_sms, int* k_slices, int* k_per_slice);

@@ -126,48 +126,75 @@ int num_sms_current() {
   return cache[dev];
 }
 
+// Tile facts of a sliceable variant: CTA tile bm x bn, k-tile bk, resident CTAs per SM.
+struct SliceTile {
+  int bm, bn, bk, occ;
+};
+
+bool slice_tile(const Variant& v, SliceTile* t) {
+  if (v.family == KP_FAMILY_SIMT) {
+    const kp::F1Entry& e = registry().f1[v.index];
+    *t = SliceTile{e.bm, e.bn, e.bk, e.occ};
+    return true;
+  }
+  if (v.family == KP_FAMILY_TF32 || v.family == KP_FAMILY_BF16) {
+    // persistent 1-CTA/SM kernel; slicing only when at most half the SMs get a tile
+    *t = SliceTile{128, kp::tc_tile_n(v.family, v.index), kp::tc_tile_k(v.family), 1};
+    return t->bn > 0;
+  }
+  return false;  // PAPER: the paper's geometry, never sliced
+}
+
+int cluster_fit(const Variant& v, int slices) {
+  if (v.family == KP_FAMILY_SIMT) return registry().f1[v.index].cluster_fit(slices);
+  return kp::tc_cluster_fit(v.family, v.index, slices);
+}
+
 // Largest cluster size <= want that the variant can co-schedule on this device
 // (cudaOccupancyMaxActiveClusters >= 1), cached per (variant, size).
-int f1_fit_slices(int index, const kp::F1Entry& e, int want) {
+int fit_slices(int id, const Variant& v, int want) {
   static std::mutex mu;
-  static std::vector<int8_t> fit;  // [index][slices]: 0 unknown, 1 fits, -1 does not
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+  static std::vector<int8_t> fit;  // [id][slices]: 0 unknown, 1 fits, -1 does not
   std::lock_guard<std::mutex> lock(mu);
-  const size_t row = (kp::kMaxKSlices + 1);
-  if (fit.empty()) fit.assign(kp::kPaperConfigs * row, 0);
+  const size_t row = kp::kMaxKSlices + 1;
+  if (fit.empty()) fit.assign(registry().variants.size() * row, 0);
   for (int s = want; s > 1; --s) {
-    int8_t& f = fit[index * row + s];
-    if (f == 0) f = e.cluster_fit(s) >= 1 ? 1 : -1;
+    int8_t& f = fit[id * row + s];
+    if (f == 0) f = cluster_fit(v, s) >= 1 ? 1 : -1;
     if (f > 0) return s;
   }
   return 1;
 }
 
-void f1_plan(const kp::F1Entry& e, int m, int k, int n, int batch, int sms, int max_slices, int* slices,
-             int* kt_per_slice) {
-  const int64_t tiles = ((m + e.bm - 1) / e.bm) * static_cast<int64_t>((n + e.bn - 1) / e.bn) * batch;
-  const int kt = (k + e.bk - 1) / e.bk;
-  const int64_t slots = static_cast<int64_t>(sms) * e.occ;
+// The k-slice plan of variant id on (m, k, n, batch): S slices of kt_per_slice k-tiles
+// (S == 1: kt_per_slice = all k-tiles).  sms > 0 with device == false plans for a
+// hypothetical device (no cluster-occupancy query).
+void plan_slices(int id, int m, int k, int n, int batch, int sms, bool device, int* slices, int* kt_per_slice,
+                 int* bk) {
+  const Variant& v = registry().variants[id];
+  SliceTile t{1, 1, k, 1};
+  const int max_slices = g_max_kslices.load(std::memory_order_relaxed);
   int s = 1;
-  if (max_slices > 1 && tiles < slots) {
-    const int64_t want = slots / tiles;
-    s = static_cast<int>(want < max_slices ? want : max_slices);
-    const int by_k = k / kMinSliceK;
-    if (s > by_k) s = by_k;
-    if (s < 1) s = 1;
+  if (slice_tile(v, &t) && max_slices > 1) {
+    const int64_t tiles = ((m + t.bm - 1) / t.bm) * static_cast<int64_t>((n + t.bn - 1) / t.bn) * batch;
+    const int64_t slots = static_cast<int64_t>(sms) * t.occ;
+    const bool underfilled = v.family == KP_FAMILY_SIMT ? tiles < slots : 2 * tiles <= slots;
+    if (underfilled) {
+      const int64_t want = slots / tiles;
+      s = static_cast<int>(want < max_slices ? want : max_slices);
+      const int by_k = k / kMinSliceK;
+      if (s > by_k) s = by_k;
+      if (s < 1) s = 1;
+      if (device && s > 1) s = fit_slices(id, v, s);
+    }
   }
-  *slices = s;
-  *kt_per_slice = kt;
-}
-
-void f1_split(int kt, int* slices, int* kt_per_slice) {
-  int s = *slices;
+  const int kt = (k + t.bk - 1) / t.bk;
   int per = (kt + s - 1) / s;
   s = (kt + per - 1) / per;  // no empty slices
   if (s == 1) per = kt;
   *slices = s;
   *kt_per_slice = per;
+  *bk = t.bk;
 }
 
 int launch(int id, const kp::GemmArgs& p0, cudaStream_t s) {
@@ -179,23 +206,19 @@ int launch(int id, const kp::GemmArgs& p0, cudaStream_t s) {
     case KP_FAMILY_PAPER:
       e = kp::f0_launch(v.choice, p, s);
       break;
-    case KP_FAMILY_SIMT: {
-      const kp::F1Entry& fe = reg.f1[v.index];
-      const int max_slices = g_max_kslices.load(std::memory_order_relaxed);
-      if (max_slices > 1) {
+    case KP_FAMILY_SIMT:
+    default: {
+      if (v.family != KP_FAMILY_SIMT) {
+        const int rc = kp::tc_check(v.family, v.index, p);
+        if (rc != KP_OK) return fail(rc, "variant %d cannot run this problem: %s", id, kp::tc_last_reason());
+      }
+      if (g_max_kslices.load(std::memory_order_relaxed) > 1) {
         const int sms = num_sms_current();
         if (sms < 1) return fail(KP_EIO, "cannot query the SM count of the current device");
-        f1_plan(fe, p.m, p.k, p.n, p.batch, sms, max_slices, &p.kslices, &p.kt_per_slice);
-        if (p.kslices > 1) p.kslices = f1_fit_slices(v.index, fe, p.kslices);
-        f1_split(p.kt_per_slice, &p.kslices, &p.kt_per_slice);
+        int bk = 0;
+        plan_slices(id, p.m, p.k, p.n, p.batch, sms, true, &p.kslices, &p.kt_per_slice, &bk);
       }
-      e = fe.launch(p, s);
-      break;
-    }
-    default: {
-      const int rc = kp::tc_check(v.family, v.index, p);
-      if (rc != KP_OK) return fail(rc, "variant %d cannot run this problem: %s", id, kp::tc_last_reason());
-      e = kp::tc_launch(v.family, v.index, p, s);
+      e = v.family == KP_FAMILY_SIMT ? reg.f1[v.index].launch(p, s) : kp::tc_launch(v.family, v.index, p, s);
       break;
     }
   }
@@ -315,24 +338,16 @@ int kp_gemm_plan(int id, int m, int k, int n, int batch, int num_sms, int* k_sli
   if (id < 0 || id >= static_cast<int>(reg.variants.size())) return fail(KP_ENOENT, "unknown variant id %d", id);
   if (m < 1 || k < 1 || n < 1 || batch < 1) return fail(KP_EINVAL, "dims must be >= 1");
   if (!k_slices || !k_per_slice) return fail(KP_EINVAL, "null output pointer");
-  const Variant& v = reg.variants[id];
-  const int max_slices = g_max_kslices.load(std::memory_order_relaxed);
-  if (v.family != KP_FAMILY_SIMT || max_slices <= 1) {
-    *k_slices = 1;
-    *k_per_slice = k;
-    return KP_OK;
-  }
   const bool device = num_sms <= 0;
-  if (device) num_sms = num_sms_current();
-  if (num_sms < 1) return fail(KP_EIO, "cannot query the SM count of the current device");
-  const kp::F1Entry& fe = reg.f1[v.index];
-  int s = 1, per = 0;
-  f1_plan(fe, m, k, n, batch, num_sms, max_slices, &s, &per);
-  if (device && s > 1) s = f1_fit_slices(v.index, fe, s);  // the device's cluster limit
-  f1_split(per, &s, &per);
+  if (device && g_max_kslices.load(std::memory_order_relaxed) > 1) {
+    num_sms = num_sms_current();
+    if (num_sms < 1) return fail(KP_EIO, "cannot query the SM count of the current device");
+  }
+  int s = 1, per = 0, bk = 1;
+  plan_slices(id, m, k, n, batch, num_sms > 0 ? num_sms : 1, device, &s, &per, &bk);
   *k_slices = s;
-  const int64_t depth = static_cast<int64_t>(per) * fe.bk;
-  *k_per_slice = static_cast<int>(depth < k ? depth : k);
+  const int64_t depth = static_cast<int64_t>(per) * bk;
+  *k_per_slice = s == 1 ? k : static_cast<int>(depth < k ? depth : k);
   return KP_OK;
 }
 

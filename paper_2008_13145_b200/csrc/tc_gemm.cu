@@ -29,12 +29,14 @@
 // Numerics: BF16 operands are exact bf16 inputs, fp32 accumulation.  TF32 reads fp32
 // operands and uses their top 19 bits (truncation), fp32 accumulation; tolerances in
 // tests/test_tc_gpu.py: |C - C64| <= (2*eps_in + 2*k*2^-24) * (|A||B|)_ij.
+#include <cooperative_groups.h>
 #include <cuda.h>
 
 #include <cstdio>
 #include <cstring>
 #include <type_traits>
 
+#include "families.h"
 #include "tc_families.h"
 
 namespace kp {
@@ -135,7 +137,11 @@ struct TcCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // two accumulators (double-buffered TMEM), power-of-two column allocation
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // k-sliced launches park the fp32 partial tile (row stride BN + 4) in the ring
+  static constexpr int PART_STRIDE = BN + 4;
+  static constexpr int PART_BYTES = BM * PART_STRIDE * 4;
+  static constexpr int RING_BYTES = STAGES * STAGE_BYTES > PART_BYTES ? STAGES * STAGE_BYTES : PART_BYTES;
+  static constexpr int SMEM_BYTES = RING_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(2 * BN <= 512, "two accumulators must fit TMEM");
   static constexpr uint32_t IDESC = (1u << 4)                      // D = f32
                                     | ((kTF32 ? 2u : 1u) << 7)     // A = tf32 / bf16
@@ -197,6 +203,48 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   n0 = (local / rows) * BN;
 }
 
+// Cluster reduction of a k-sliced launch (grid = (#tiles, 1, S), cluster (1, 1, S), one
+// tile per CTA): CTA rank z sums elements [z*chunk, (z+1)*chunk) of the 128 x BN tile
+// over every rank's shared-memory partial (DSMEM) in rank order, then applies the
+// epilogue and stores.  Same slice order as the SIMT family: ((p0 + p1) + p2) + ...
+template <int BN>
+__device__ __forceinline__ void tc_slice_reduce(const GemmArgs& p, float* part, int tiles_m, int tiles_n) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();
+  int b, m0, n0;
+  tile_coords<BN>(blockIdx.x, tiles_m, tiles_n, b, m0, n0);
+  constexpr int PS = BN + 4, Q = BN / 4, TOT = BM * Q;
+  const int S = p.kslices, z = static_cast<int>(cl.block_rank());
+  const int chunk = (TOT + S - 1) / S, end = min(TOT, (z + 1) * chunk);
+  float* Cb = static_cast<float*>(p.C) + static_cast<int64_t>(b) * p.sC;
+  for (int i = z * chunk + static_cast<int>(threadIdx.x); i < end; i += kThreads) {
+    const int r = i / Q, c = (i - r * Q) * 4;
+    const int row = m0 + r, col = n0 + c;
+    if (row >= p.m || col >= p.n) continue;
+    float4 v = *reinterpret_cast<const float4*>(cl.map_shared_rank(part, 0) + r * PS + c);
+    for (int s = 1; s < S; ++s) {
+      const float4 w = *reinterpret_cast<const float4*>(cl.map_shared_rank(part, s) + r * PS + c);
+      v.x = v.x + w.x; v.y = v.y + w.y; v.z = v.z + w.z; v.w = v.w + w.w;
+    }
+    float o[4] = {v.x, v.y, v.z, v.w};
+    if (p.bias || p.relu) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (col + e < p.n) o[e] = epilogue(p, o[e], col + e);
+    }
+    float* out = Cb + static_cast<int64_t>(row) * p.ldc + col;
+    if (p.c_vec && col + 4 <= p.n) {
+      *reinterpret_cast<float4*>(out) = make_float4(o[0], o[1], o[2], o[3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (col + e < p.n) out[e] = o[e];
+    }
+  }
+  cl.sync();  // keep this CTA's partial alive until every rank has read it
+}
+
 // Persistent: gridDim.x = min(#tiles, #SMs) CTAs walk the tile list (tile_coords
 // order, then batch) with stride gridDim.x.  The smem ring runs continuously across tiles
 // and TMEM holds two accumulators, so the epilogue of tile i overlaps the MMAs of
@@ -208,14 +256,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   using Cfg = TcCfg<kTF32, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::RING_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;  // [2]
   uint64_t* tmem_empty = tmem_full + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int KT = (p.k + Cfg::BK - 1) / Cfg::BK;
+  // this CTA's k-tiles: all of them, or slice blockIdx.z of a k-sliced launch
+  const int kt0 = static_cast<int>(blockIdx.z) * p.kt_per_slice;
+  const int KT = min((p.k + Cfg::BK - 1) / Cfg::BK - kt0, p.kt_per_slice);
+  const bool sliced = p.kslices > 1;
   const int per_batch = tiles_m * tiles_n;
   const int n_tiles = per_batch * p.batch;
 
@@ -257,10 +308,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
         uint8_t* sb = sa + Cfg::A_BYTES;
         mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
-        tma_load_3d(sa, &mapA, &full[s], kt * Cfg::BK, m0, za);
+        tma_load_3d(sa, &mapA, &full[s], (kt0 + kt) * Cfg::BK, m0, za);
 #pragma unroll
         for (int j = 0; j < BN / Cfg::NATOM; ++j)
-          tma_load_3d(sb + j * (Cfg::BK * 128), &mapB, &full[s], n0 + j * Cfg::NATOM, kt * Cfg::BK, zb);
+          tma_load_3d(sb + j * (Cfg::BK * 128), &mapB, &full[s], n0 + j * Cfg::NATOM, (kt0 + kt) * Cfg::BK, zb);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -301,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
-          lsu_stage<kTF32, BN>(sa, sa + Cfg::A_BYTES, p, b, m0, n0, kt * Cfg::BK, tid);
+          lsu_stage<kTF32, BN>(sa, sa + Cfg::A_BYTES, p, b, m0, n0, (kt0 + kt) * Cfg::BK, tid);
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
         }
       }
@@ -310,11 +361,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int row = m0 + quad * 32 + lane;
       float* out = static_cast<float*>(p.C) + static_cast<int64_t>(b) * p.sC + static_cast<int64_t>(row) * p.ldc;
+      // k-sliced: the accumulator goes to this CTA's partial tile in shared memory (the
+      // ring is idle: tmem_full means every MMA, and so every smem read, has finished)
+      float* part = reinterpret_cast<float*>(smem) + (quad * 32 + lane) * Cfg::PART_STRIDE;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         float v[16];
         tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * BN + c, v);
-        if (row < p.m) {
+        if (sliced) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<float4*>(part + c + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else if (row < p.m) {
           const int col = n0 + c;
           if (p.bias || p.relu) {
 #pragma unroll
@@ -344,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
   }
+  if (sliced) tc_slice_reduce<BN>(p, reinterpret_cast<float*>(smem), tiles_m, tiles_n);
 }
 
 // ---------------------------------------------------------------- host side --
@@ -406,11 +465,11 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   using Cfg = TcCfg<kTF32, BN, STAGES>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<kTF32, BN, STAGES, false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(tc_gemm_kernel<kTF32, BN, STAGES, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               Cfg::SMEM_BYTES);
+    cudaError_t e = cudaSuccess;
+    for (auto fn : {tc_gemm_kernel<kTF32, BN, STAGES, false>, tc_gemm_kernel<kTF32, BN, STAGES, true>}) {
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -420,13 +479,31 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   const int tiles_m = (p.m + BM - 1) / BM, tiles_n = (p.n + BN - 1) / BN;
   const int64_t n_tiles = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
   if (n_tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  dim3 grid(static_cast<unsigned>(n_tiles < num_sms() ? n_tiles : num_sms()));
+  const int KT = (p.k + Cfg::BK - 1) / Cfg::BK;
+  if (p.kslices <= 1) {
+    p.kslices = 1;
+    p.kt_per_slice = KT;
+  } else if (p.kslices > kMaxKSlices || n_tiles > num_sms()) {
+    return cudaErrorInvalidConfiguration;  // sliced launches run one tile per CTA
+  }
+  // k-sliced: grid (#tiles, 1, S) in (1, 1, S) clusters; else persistent over the SMs
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = p.kslices > 1 ? dim3(static_cast<unsigned>(n_tiles), 1, p.kslices)
+                             : dim3(static_cast<unsigned>(n_tiles < num_sms() ? n_tiles : num_sms()));
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = p.kslices;
+  lc.attrs = at;
+  lc.numAttrs = p.kslices > 1 ? 1 : 0;
   if (!tma_ok(p, Cfg::ES)) {
     CUtensorMap dummy;
     std::memset(&dummy, 0, sizeof(dummy));
-    tc_gemm_kernel<kTF32, BN, STAGES, true><<<grid, kThreads, Cfg::SMEM_BYTES, s>>>(dummy, dummy, p, tiles_m, tiles_n,
-                                                                                   0, 0);
-    return cudaGetLastError();
+    return cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, true>, dummy, dummy, p, tiles_m, tiles_n, 0, 0);
   }
   EncodeFn enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
@@ -459,9 +536,57 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  tc_gemm_kernel<kTF32, BN, STAGES, false><<<grid, kThreads, Cfg::SMEM_BYTES, s>>>(ma, mb, p, tiles_m, tiles_n,
-                                                                                   a_batched, b_batched);
-  return cudaGetLastError();
+  return cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, false>, ma, mb, p, tiles_m, tiles_n, a_batched,
+                            b_batched);
+}
+
+// cudaOccupancyMaxActiveClusters of a (1, 1, slices) cluster launch (< 0: error).
+template <bool kTF32, int BN, int STAGES>
+int cluster_fit_tc(int slices) {
+  using Cfg = TcCfg<kTF32, BN, STAGES>;
+  for (auto fn : {tc_gemm_kernel<kTF32, BN, STAGES, false>, tc_gemm_kernel<kTF32, BN, STAGES, true>})
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      return -1;
+    }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(1, 1, slices);
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = slices;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_kernel<kTF32, BN, STAGES, false>, &lc) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return n;
+}
+
+template <bool kTF32>
+int dispatch_fit(const TcConfig& c, int slices) {
+  switch (c.bn * 16 + c.stages) {
+    case 32 * 16 + 4:
+      if constexpr (kTF32) return cluster_fit_tc<kTF32, 32, 4>(slices);
+      return -1;
+    case 64 * 16 + 4: return cluster_fit_tc<kTF32, 64, 4>(slices);
+    case 128 * 16 + 4: return cluster_fit_tc<kTF32, 128, 4>(slices);
+    case 256 * 16 + 4: return cluster_fit_tc<kTF32, 256, 4>(slices);
+    case 64 * 16 + 8: return cluster_fit_tc<kTF32, 64, 8>(slices);
+    case 128 * 16 + 6: return cluster_fit_tc<kTF32, 128, 6>(slices);
+    case 256 * 16 + 3: return cluster_fit_tc<kTF32, 256, 3>(slices);
+    case 128 * 16 + 2:
+      if constexpr (!kTF32) return cluster_fit_tc<kTF32, 128, 2>(slices);
+      return -1;
+    case 192 * 16 + 4: return cluster_fit_tc<kTF32, 192, 4>(slices);
+    default: return -1;
+  }
 }
 
 template <bool kTF32>
@@ -503,6 +628,19 @@ int tc_check(int family, int index, const GemmArgs& p) {
     return KP_ENOENT;
   }
   return KP_OK;
+}
+
+int tc_tile_n(int family, int index) {
+  const TcConfig* c = config_of(family, index);
+  return c ? c->bn : -1;
+}
+
+int tc_tile_k(int family) { return family == KP_FAMILY_TF32 ? 32 : 64; }
+
+int tc_cluster_fit(int family, int index, int slices) {
+  const TcConfig* c = config_of(family, index);
+  if (!c) return -1;
+  return c->tf32 ? dispatch_fit<true>(*c, slices) : dispatch_fit<false>(*c, slices);
 }
 
 cudaError_t tc_launch(int family, int index, const GemmArgs& p, cudaStream_t s) {

@@ -61,3 +61,49 @@ def test_unaligned_rows_use_lsu_staging(cuda_device, fam, m, k, n, batch):
     the LSU staging path with the same tolerance (grid totality, dataset.py:259-264)."""
     for cfg in gemm.family_configs(fam)[::2]:
         _check(fam, cfg, m, k, n, batch, cuda_device, bcast=(batch > 1), seed=k)
+
+
+@pytest.mark.parametrize("fam", ["bf16", "tf32"])
+@pytest.mark.parametrize("m,k,n,batch", [(196, 4608, 512, 1), (32, 25088, 1024, 1), (100, 3000, 200, 2),
+                                         (64, 1001, 64, 1), (128, 2048, 33, 1)])
+def test_k_sliced_tensor_core(cuda_device, fam, m, k, n, batch):
+    """Under-filled launches slice k over a thread-block cluster (kp_gemm_plan) and sum
+    the slices through DSMEM: every config within the bound, deterministic run to run
+    (k = 1001 and n = 33 rows are unaligned, so they also exercise LSU staging)."""
+    from paper_2008_13145_b200.dataset import ProblemSize
+    sliced = 0
+    for cfg in gemm.family_configs(fam):
+        s, kps = gemm.k_slice_plan(cfg, ProblemSize(m, k, n, batch), family=fam)
+        sliced += s > 1
+        _check(fam, cfg, m, k, n, batch, cuda_device, bcast=(batch > 1), seed=k)
+    assert sliced > 0
+    g = torch.Generator(device=cuda_device).manual_seed(9)
+    A = torch.rand(m, k, device=cuda_device, generator=g)
+    B = torch.rand(k, n, device=cuda_device, generator=g)
+    if fam == "bf16":
+        A, B = A.bfloat16(), B.bfloat16()
+    cfg = gemm.family_configs(fam)[1]
+    assert torch.equal(gemm.matmul(A, B, cfg, fam), gemm.matmul(A, B, cfg, fam))
+
+
+@pytest.mark.parametrize("fam", ["bf16", "tf32"])
+def test_k_sliced_epilogue(cuda_device, fam):
+    """bias + ReLU applied once, after the slice sum."""
+    from paper_2008_13145_b200 import _lib
+    from paper_2008_13145_b200.dataset import ProblemSize
+    m, k, n = 200, 4096, 256
+    g = torch.Generator(device=cuda_device).manual_seed(4)
+    A = torch.rand(m, k, device=cuda_device, generator=g) * 2 - 1
+    B = torch.rand(k, n, device=cuda_device, generator=g) * 2 - 1
+    bias = torch.rand(n, device=cuda_device, generator=g) * 2 - 1
+    if fam == "bf16":
+        A, B = A.bfloat16(), B.bfloat16()
+    cfg = gemm.family_configs(fam)[2]
+    assert gemm.k_slice_plan(cfg, ProblemSize(m, k, n, 1), family=fam)[0] > 1
+    plain = gemm.matmul(A, B, cfg, fam)
+    C = torch.empty(m, n, device=cuda_device)
+    vid = gemm.variant_id(cfg, fam)
+    _lib.check(_lib.load().kp_gemm_ex(vid, m, k, n, 1, A.data_ptr(), k, 0, B.data_ptr(), n, 0, C.data_ptr(), n, 0,
+                                      bias.data_ptr(), _lib.KP_EPI_RELU, torch.cuda.current_stream().cuda_stream),
+               "kp_gemm_ex")
+    assert torch.equal(C, torch.relu(plain + bias))
