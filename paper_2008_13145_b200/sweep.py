@@ -269,7 +269,8 @@ def write_benchmark_csv(pm: PerfMatrix, path: str | os.PathLike) -> None:
     os.replace(tmp, path)
 
 
-def _problem_set(name: str, batches) -> list[ProblemSize]:
+def problem_set(name: str, batches=(1, 2, 4, 8, 16, 32, 64)) -> list[ProblemSize]:
+    """Named sweep shape sets: vgg16 / resnet50 (conv-as-GEMM x batches), square, square16k."""
     from . import shapes
 
     if name in shapes.NETWORKS:
@@ -296,7 +297,7 @@ def main(argv=None) -> int:
     ap.add_argument("--work", default=None, help="shard/partial directory (default: <out>.parts)")
     ap.add_argument("--min-ms", type=float, default=3.0)
     args = ap.parse_args(argv)
-    problems = _problem_set(args.set, tuple(int(b) for b in args.batches.split(",")))
+    problems = problem_set(args.set, tuple(int(b) for b in args.batches.split(",")))
     work = Path(args.work or (args.out + ".parts"))
     t0 = time.time()
     last = [0.0]

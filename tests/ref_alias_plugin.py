@@ -5,7 +5,8 @@ host-side restatement.  Test infrastructure only."""
 import importlib
 import sys
 
-MODULES = ("errors", "dataset", "normalize", "pca", "selection", "classify", "evaluate", "codegen")
+MODULES = ("errors", "dataset", "normalize", "pca", "selection", "classify", "evaluate", "codegen", "pipeline",
+           "cli")
 
 
 def pytest_load_initial_conftests(early_config, parser, args):

@@ -84,3 +84,24 @@ def test_shape_sets():
     allv = shapes.network_problems("vgg16")
     assert len(allv) == len(set(allv))
     assert ProblemSize(784, 4608, 512, 1) in allv  # conv4_2 @1 == conv5 @4 kept once
+
+
+def test_cli_sweep_usage_and_config_keys(tmp_path, capsys):
+    """CPU side of the CLI additions: flags parse, sweep keys are accepted in a run
+    config, unknown keys still exit 2, usage errors exit 1 (cli.py:36-43)."""
+    import json
+
+    from paper_2008_13145_b200 import cli
+    from paper_2008_13145_b200.pipeline import PipelineConfig
+
+    args = cli.build_parser().parse_args(["sweep", "--set", "resnet50", "--batches", "1,2", "--family", "simt+tf32",
+                                          "--gpus", "8", "--output", "x.csv"])
+    assert args.batches == (1, 2) and args.gpus == 8 and args.func is cli.cmd_sweep
+    assert cli.main(["sweep"]) == 1  # --output is required
+    cfg = PipelineConfig(sweep_set="vgg16", sweep_family="bf16", sweep_gpus=2)
+    assert cfg.sweep_gpus == 2
+    with pytest.raises(ValueError):
+        PipelineConfig(sweep_gpus=0)
+    bad = tmp_path / "cfg.json"
+    bad.write_text(json.dumps({"sweep_sets": "vgg16"}))
+    assert cli.main(["run", "--config", str(bad), "--output-dir", str(tmp_path / "o")]) == 2
