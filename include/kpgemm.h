@@ -105,9 +105,10 @@ int kp_gemm_ex(int id, int m, int k, int n, int batch,
  * A launch whose output tiles cannot fill the GPU's resident-CTA slots (SIMT: SM count
  * x the config's occupancy target; tensor-core families: at most half the SMs get a
  * tile) cuts k into S <= 8 consecutive slices (each at
- * least 256 deep, aligned to the config's k-tile) computed by the CTAs of one
- * (1, 1, S) thread-block cluster (S is lowered to what cudaOccupancyMaxActiveClusters
- * can co-schedule on the current device; the cap can be raised to the non-portable
+ * least 256 (SIMT) / 768 (TF32, BF16) deep, aligned to the config's k-tile) computed by
+ * the CTAs of one (1, 1, S) thread-block cluster per output tile (S is lowered until
+ * cudaOccupancyMaxActiveClusters can co-schedule every tile's cluster in one wave on
+ * the current device; the cap can be raised to the non-portable
  * cluster limit 16 with kp_set_max_k_slices); each output is then the fp32 fma chain
  * over every slice, summed in slice order ((p0 + p1) + p2) + ... through distributed
  * shared memory -- deterministic for a given (config, shape, device).

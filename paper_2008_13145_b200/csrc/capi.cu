@@ -109,7 +109,8 @@ int check_problem(int id, int m, int k, int n, int batch, const void* A, int64_t
 // a pure function of (config, shape, SM count), so results are deterministic on a
 // given GPU model and the oracle reproduces them from kp_gemm_plan.
 std::atomic<int> g_max_kslices{kp::kDefaultKSlices};
-constexpr int kMinSliceK = 256;  // never cut k into slices shallower than this
+constexpr int kMinSliceK = 256;    // never cut k into slices shallower than this (SIMT)
+constexpr int kMinSliceKTc = 768;  // tensor cores: shallower slices lose to the fixed costs
 
 int num_sms_current() {
   static std::mutex mu;
@@ -150,18 +151,19 @@ int cluster_fit(const Variant& v, int slices) {
   return kp::tc_cluster_fit(v.family, v.index, slices);
 }
 
-// Largest cluster size <= want that the variant can co-schedule on this device
-// (cudaOccupancyMaxActiveClusters >= 1), cached per (variant, size).
-int fit_slices(int id, const Variant& v, int want) {
+// Largest cluster size s <= want for which the device can co-schedule `clusters`
+// (1, 1, s) clusters of this variant at once (cudaOccupancyMaxActiveClusters), so a
+// sliced launch stays a single wave; cached per (variant, size).
+int fit_slices(int id, const Variant& v, int want, int64_t clusters) {
   static std::mutex mu;
-  static std::vector<int8_t> fit;  // [id][slices]: 0 unknown, 1 fits, -1 does not
+  static std::vector<int> fit;  // [id][slices]: max active clusters, -2 = not queried yet
   std::lock_guard<std::mutex> lock(mu);
   const size_t row = kp::kMaxKSlices + 1;
-  if (fit.empty()) fit.assign(registry().variants.size() * row, 0);
+  if (fit.empty()) fit.assign(registry().variants.size() * row, -2);
   for (int s = want; s > 1; --s) {
-    int8_t& f = fit[id * row + s];
-    if (f == 0) f = cluster_fit(v, s) >= 1 ? 1 : -1;
-    if (f > 0) return s;
+    int& f = fit[id * row + s];
+    if (f == -2) f = cluster_fit(v, s);
+    if (f >= clusters) return s;
   }
   return 1;
 }
@@ -182,10 +184,10 @@ void plan_slices(int id, int m, int k, int n, int batch, int sms, bool device, i
     if (underfilled) {
       const int64_t want = slots / tiles;
       s = static_cast<int>(want < max_slices ? want : max_slices);
-      const int by_k = k / kMinSliceK;
+      const int by_k = k / (v.family == KP_FAMILY_SIMT ? kMinSliceK : kMinSliceKTc);
       if (s > by_k) s = by_k;
       if (s < 1) s = 1;
-      if (device && s > 1) s = fit_slices(id, v, s);
+      if (device && s > 1) s = fit_slices(id, v, s, tiles);
     }
   }
   const int kt = (k + t.bk - 1) / t.bk;

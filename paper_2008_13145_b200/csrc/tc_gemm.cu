@@ -140,8 +140,10 @@ struct TcCfg {
   // k-sliced launches park the fp32 partial tile (row stride BN + 4) in the ring
   static constexpr int PART_STRIDE = BN + 4;
   static constexpr int PART_BYTES = BM * PART_STRIDE * 4;
-  static constexpr int RING_BYTES = STAGES * STAGE_BYTES > PART_BYTES ? STAGES * STAGE_BYTES : PART_BYTES;
+  static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
+  static constexpr int SLICED_RING_BYTES = RING_BYTES > PART_BYTES ? RING_BYTES : PART_BYTES;
   static constexpr int SMEM_BYTES = RING_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SLICED_SMEM_BYTES = SLICED_RING_BYTES + 1024 + 256;
   static_assert(2 * BN <= 512, "two accumulators must fit TMEM");
   static constexpr uint32_t IDESC = (1u << 4)                      // D = f32
                                     | ((kTF32 ? 2u : 1u) << 7)     // A = tf32 / bf16
@@ -150,7 +152,7 @@ struct TcCfg {
                                     | (1u << 16)                   // B MN-major
                                     | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
   static_assert(BN % NATOM == 0 && BN >= 16 && BN <= 256, "tile N");
-  static_assert(SMEM_BYTES <= 227 * 1024, "smem");
+  static_assert(SLICED_SMEM_BYTES <= 227 * 1024, "smem");
 };
 
 // LSU staging (operands whose rows are not 16-byte aligned, e.g. k = 27 or 147, so
@@ -249,14 +251,14 @@ __device__ __forceinline__ void tc_slice_reduce(const GemmArgs& p, float* part, 
 // order, then batch) with stride gridDim.x.  The smem ring runs continuously across tiles
 // and TMEM holds two accumulators, so the epilogue of tile i overlaps the MMAs of
 // tile i+1 (tmem_full / tmem_empty mbarrier pairs).
-template <bool kTF32, int BN, int STAGES, bool kLsu>
+template <bool kTF32, int BN, int STAGES, bool kLsu, bool kSliced>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, GemmArgs p,
                    int tiles_m, int tiles_n, int a_batched, int b_batched) {
   using Cfg = TcCfg<kTF32, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::RING_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (kSliced ? Cfg::SLICED_RING_BYTES : Cfg::RING_BYTES));
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;  // [2]
   uint64_t* tmem_empty = tmem_full + 2;  // [2]
@@ -264,9 +266,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // this CTA's k-tiles: all of them, or slice blockIdx.z of a k-sliced launch
-  const int kt0 = static_cast<int>(blockIdx.z) * p.kt_per_slice;
-  const int KT = min((p.k + Cfg::BK - 1) / Cfg::BK - kt0, p.kt_per_slice);
-  const bool sliced = p.kslices > 1;
+  // (kSliced is a separate instantiation so the persistent kernel keeps its own code)
+  const int kt0 = kSliced ? static_cast<int>(blockIdx.z) * p.kt_per_slice : 0;
+  const int KT = kSliced ? min((p.k + Cfg::BK - 1) / Cfg::BK - kt0, p.kt_per_slice) : (p.k + Cfg::BK - 1) / Cfg::BK;
+  constexpr bool sliced = kSliced;
   const int per_batch = tiles_m * tiles_n;
   const int n_tiles = per_batch * p.batch;
 
@@ -368,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < BN; c += 16) {
         float v[16];
         tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * BN + c, v);
-        if (sliced) {
+        if constexpr (sliced) {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             *reinterpret_cast<float4*>(part + c + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
   }
-  if (sliced) tc_slice_reduce<BN>(p, reinterpret_cast<float*>(smem), tiles_m, tiles_n);
+  if constexpr (sliced) tc_slice_reduce<BN>(p, reinterpret_cast<float*>(smem), tiles_m, tiles_n);
 }
 
 // ---------------------------------------------------------------- host side --
@@ -466,8 +469,11 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaSuccess;
-    for (auto fn : {tc_gemm_kernel<kTF32, BN, STAGES, false>, tc_gemm_kernel<kTF32, BN, STAGES, true>}) {
+    for (auto fn : {tc_gemm_kernel<kTF32, BN, STAGES, false, false>, tc_gemm_kernel<kTF32, BN, STAGES, true, false>})
       if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    for (auto fn : {tc_gemm_kernel<kTF32, BN, STAGES, false, true>, tc_gemm_kernel<kTF32, BN, STAGES, true, true>}) {
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SLICED_SMEM_BYTES);
       if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     }
     if (e != cudaSuccess) return e;
@@ -491,7 +497,7 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   lc.gridDim = p.kslices > 1 ? dim3(static_cast<unsigned>(n_tiles), 1, p.kslices)
                              : dim3(static_cast<unsigned>(n_tiles < num_sms() ? n_tiles : num_sms()));
   lc.blockDim = dim3(kThreads);
-  lc.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  lc.dynamicSmemBytes = p.kslices > 1 ? Cfg::SLICED_SMEM_BYTES : Cfg::SMEM_BYTES;
   lc.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -503,7 +509,11 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   if (!tma_ok(p, Cfg::ES)) {
     CUtensorMap dummy;
     std::memset(&dummy, 0, sizeof(dummy));
-    return cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, true>, dummy, dummy, p, tiles_m, tiles_n, 0, 0);
+    return p.kslices > 1
+               ? cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, true, true>, dummy, dummy, p, tiles_m, tiles_n,
+                                    0, 0)
+               : cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, true, false>, dummy, dummy, p, tiles_m,
+                                    tiles_n, 0, 0);
   }
   EncodeFn enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
@@ -536,16 +546,18 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  return cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, false>, ma, mb, p, tiles_m, tiles_n, a_batched,
-                            b_batched);
+  return p.kslices > 1 ? cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, false, true>, ma, mb, p, tiles_m,
+                                            tiles_n, a_batched, b_batched)
+                      : cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, false, false>, ma, mb, p, tiles_m,
+                                           tiles_n, a_batched, b_batched);
 }
 
 // cudaOccupancyMaxActiveClusters of a (1, 1, slices) cluster launch (< 0: error).
 template <bool kTF32, int BN, int STAGES>
 int cluster_fit_tc(int slices) {
   using Cfg = TcCfg<kTF32, BN, STAGES>;
-  for (auto fn : {tc_gemm_kernel<kTF32, BN, STAGES, false>, tc_gemm_kernel<kTF32, BN, STAGES, true>})
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) != cudaSuccess ||
+  for (auto fn : {tc_gemm_kernel<kTF32, BN, STAGES, false, true>, tc_gemm_kernel<kTF32, BN, STAGES, true, true>})
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SLICED_SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
       cudaGetLastError();
       return -1;
@@ -553,7 +565,7 @@ int cluster_fit_tc(int slices) {
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(1, 1, slices);
   lc.blockDim = dim3(kThreads);
-  lc.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  lc.dynamicSmemBytes = Cfg::SLICED_SMEM_BYTES;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 1;
@@ -562,7 +574,7 @@ int cluster_fit_tc(int slices) {
   lc.attrs = at;
   lc.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_kernel<kTF32, BN, STAGES, false>, &lc) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_kernel<kTF32, BN, STAGES, false, true>, &lc) != cudaSuccess) {
     cudaGetLastError();
     return -1;
   }

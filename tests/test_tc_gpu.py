@@ -65,11 +65,11 @@ def test_unaligned_rows_use_lsu_staging(cuda_device, fam, m, k, n, batch):
 
 @pytest.mark.parametrize("fam", ["bf16", "tf32"])
 @pytest.mark.parametrize("m,k,n,batch", [(196, 4608, 512, 1), (32, 25088, 1024, 1), (100, 3000, 200, 2),
-                                         (64, 1001, 64, 1), (128, 2048, 33, 1)])
+                                         (64, 2001, 64, 1), (128, 2048, 33, 1)])
 def test_k_sliced_tensor_core(cuda_device, fam, m, k, n, batch):
     """Under-filled launches slice k over a thread-block cluster (kp_gemm_plan) and sum
     the slices through DSMEM: every config within the bound, deterministic run to run
-    (k = 1001 and n = 33 rows are unaligned, so they also exercise LSU staging)."""
+    (k = 2001 and n = 33 rows are unaligned, so they also exercise LSU staging)."""
     from paper_2008_13145_b200.dataset import ProblemSize
     sliced = 0
     for cfg in gemm.family_configs(fam):
