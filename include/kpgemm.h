@@ -104,7 +104,8 @@ int kp_gemm_ex(int id, int m, int k, int n, int batch,
 /* ---- k-slicing (SIMT, TF32 and BF16 families) ----------------------------
  * A launch whose output tiles cannot fill the GPU's resident-CTA slots (SIMT: SM count
  * x the config's occupancy target; tensor-core families: at most half the SMs get a
- * tile) cuts k into S <= 8 consecutive slices (each at
+ * tile) cuts k into S <= 8 consecutive slices (SIMT launches of 1 to 3 waves with
+ * k >= 512 use S = 2, which shrinks the partial last wave) (each at
  * least 256 (SIMT) / 768 (TF32, BF16) deep, aligned to the config's k-tile) computed by
  * the CTAs of one (1, 1, S) thread-block cluster per output tile (S is lowered until
  * cudaOccupancyMaxActiveClusters can co-schedule every tile's cluster in one wave on

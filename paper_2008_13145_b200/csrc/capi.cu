@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -188,6 +189,11 @@ void plan_slices(int id, int m, int k, int n, int batch, int sms, bool device, i
       if (s > by_k) s = by_k;
       if (s < 1) s = 1;
       if (device && s > 1) s = fit_slices(id, v, s, tiles);
+    } else if (v.family == KP_FAMILY_SIMT && tiles < 3 * slots && k >= 2 * kMinSliceK) {
+      // 1-3 waves: pairs of half-k CTAs shrink the partial last wave (measured +5-10 %
+      // at 1.3 and 2.7 waves, neutral beyond; tools/wave_probe.py)
+      s = max_slices < 2 ? max_slices : 2;
+      if (device && s > 1) s = fit_slices(id, v, s, 1);
     }
   }
   const int kt = (k + t.bk - 1) / t.bk;
@@ -219,6 +225,15 @@ int launch(int id, const kp::GemmArgs& p0, cudaStream_t s) {
         if (sms < 1) return fail(KP_EIO, "cannot query the SM count of the current device");
         int bk = 0;
         plan_slices(id, p.m, p.k, p.n, p.batch, sms, true, &p.kslices, &p.kt_per_slice, &bk);
+        static const int forced = [] {  // dev-only override for planner experiments
+          const char* e = std::getenv("KPGEMM_FORCE_SLICES");
+          return e ? std::atoi(e) : 0;
+        }();
+        if (forced > 0) {
+          const int kt = (p.k + bk - 1) / bk;
+          p.kt_per_slice = (kt + forced - 1) / forced;
+          p.kslices = (kt + p.kt_per_slice - 1) / p.kt_per_slice;
+        }
       }
       e = v.family == KP_FAMILY_SIMT ? reg.f1[v.index].launch(p, s) : kp::tc_launch(v.family, v.index, p, s);
       break;

@@ -489,8 +489,8 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   if (p.kslices <= 1) {
     p.kslices = 1;
     p.kt_per_slice = KT;
-  } else if (p.kslices > kMaxKSlices || n_tiles > num_sms()) {
-    return cudaErrorInvalidConfiguration;  // sliced launches run one tile per CTA
+  } else if (p.kslices > kMaxKSlices || n_tiles * p.kslices > 0x7fffffffLL) {
+    return cudaErrorInvalidConfiguration;  // sliced launches run one (tile, slice) per CTA
   }
   // k-sliced: grid (#tiles, 1, S) in (1, 1, S) clusters; else persistent over the SMs
   cudaLaunchConfig_t lc = {};
