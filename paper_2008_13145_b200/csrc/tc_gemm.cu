@@ -43,6 +43,7 @@ namespace kp {
 namespace {
 
 constexpr int kThreads = 192;
+constexpr int kTmaStoreMaxK = 2048;
 constexpr int BM = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -74,6 +75,17 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
+
+// TMA store of a 32 x 32 fp32 box (128B-swizzled smem) to C at (x = col, y = row, z = batch).
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -142,7 +154,11 @@ struct TcCfg {
   static constexpr int PART_BYTES = BM * PART_STRIDE * 4;
   static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
   static constexpr int SLICED_RING_BYTES = RING_BYTES > PART_BYTES ? RING_BYTES : PART_BYTES;
-  static constexpr int SMEM_BYTES = RING_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // persistent launches stage the epilogue through smem for TMA stores: per epilogue
+  // warp two 32 x 32 fp32 boxes (128B swizzle), 32 KB in all, after the barriers
+  static constexpr int EPI_OFFSET = RING_BYTES + 1024;  // 1024-aligned (swizzle atoms)
+  static constexpr int EPI_BYTES = 4 * 2 * 32 * 32 * 4;
+  static constexpr int SMEM_BYTES = EPI_OFFSET + EPI_BYTES + 1024 /*align*/;
   static constexpr int SLICED_SMEM_BYTES = SLICED_RING_BYTES + 1024 + 256;
   static_assert(2 * BN <= 512, "two accumulators must fit TMEM");
   static constexpr uint32_t IDESC = (1u << 4)                      // D = f32
@@ -152,7 +168,7 @@ struct TcCfg {
                                     | (1u << 16)                   // B MN-major
                                     | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
   static_assert(BN % NATOM == 0 && BN >= 16 && BN <= 256, "tile N");
-  static_assert(SLICED_SMEM_BYTES <= 227 * 1024, "smem");
+  static_assert(SLICED_SMEM_BYTES <= 227 * 1024 && SMEM_BYTES <= 227 * 1024, "smem");
 };
 
 // LSU staging (operands whose rows are not 16-byte aligned, e.g. k = 27 or 147, so
@@ -253,8 +269,9 @@ __device__ __forceinline__ void tc_slice_reduce(const GemmArgs& p, float* part, 
 // tile i+1 (tmem_full / tmem_empty mbarrier pairs).
 template <bool kTF32, int BN, int STAGES, bool kLsu, bool kSliced>
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, GemmArgs p,
-                   int tiles_m, int tiles_n, int a_batched, int b_batched) {
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                   const __grid_constant__ CUtensorMap mapC, GemmArgs p, int tiles_m, int tiles_n, int a_batched,
+                   int b_batched, int tma_store) {
   using Cfg = TcCfg<kTF32, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -345,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 2) {
     // ---------------- epilogue (and LSU producer for unaligned operands) ----------------
     const int quad = warp & 3;
-    int it = 0, i = 0;
+    int it = 0, i = 0, epi_box = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
       int b, m0, n0;
       tile_coords<BN>(t, tiles_m, tiles_n, b, m0, n0);
@@ -367,6 +384,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       // k-sliced: the accumulator goes to this CTA's partial tile in shared memory (the
       // ring is idle: tmem_full means every MMA, and so every smem read, has finished)
       float* part = reinterpret_cast<float*>(smem) + (quad * 32 + lane) * Cfg::PART_STRIDE;
+      if (!sliced && tma_store) {
+        // TMEM -> registers -> 128B-swizzled smem box (lane = row, conflict-free float4
+        // stores) -> one TMA store per 32 x 32 box; two boxes per warp in flight
+        uint8_t* stage = smem + Cfg::EPI_OFFSET + quad * (2 * 32 * 32 * 4);
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32, ++epi_box) {
+          float v[32];
+          tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * BN + c, v);
+          tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * BN + c + 16, v + 16);
+          if (p.bias || p.relu) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (n0 + c + e < p.n) v[e] = epilogue(p, v[e], n0 + c + e);
+          }
+          uint8_t* box = stage + (epi_box & 1) * (32 * 32 * 4);
+          if (lane == 0) bulk_wait_read<1>();  // the store that last used this box has read it
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&mapC, box, n0 + c, m0 + quad * 32, b);
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[a])) : "memory");
+        continue;
+      }
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         float v[16];
@@ -399,6 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[a])) : "memory");
     }
   }
+  if (warp >= 2 && lane == 0 && !sliced && tma_store) bulk_wait_all();  // staged boxes written out
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -506,17 +557,36 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   at[0].val.clusterDim.z = p.kslices;
   lc.attrs = at;
   lc.numAttrs = p.kslices > 1 ? 1 : 0;
+  EncodeFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  // C as a TMA store target: persistent launches with 16-byte-aligned C rows and a short
+  // k, where the epilogue is a large share of the tile (measured: 16384x64x16384 2.2x,
+  // 6272x1152x256 +15 %); with long k the stores compete with the operand loads for the
+  // TMA unit and direct stores measured slightly faster (profiles/r1_tc_epilogue.md)
+  CUtensorMap mc;
+  std::memset(&mc, 0, sizeof(mc));
+  int tma_store = 0;
+  if (p.kslices <= 1 && p.c_vec && p.k <= kTmaStoreMaxK) {
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.n), static_cast<cuuint64_t>(p.m),
+                          static_cast<cuuint64_t>(p.batch)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.ldc) * 4,
+                             static_cast<cuuint64_t>(p.batch > 1 ? p.sC : p.ldc * p.m) * 4};
+    if (p.batch == 1) strides[1] = (strides[1] + 15) / 16 * 16;
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    tma_store = enc(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, p.C, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   if (!tma_ok(p, Cfg::ES)) {
     CUtensorMap dummy;
     std::memset(&dummy, 0, sizeof(dummy));
     return p.kslices > 1
-               ? cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, true, true>, dummy, dummy, p, tiles_m, tiles_n,
-                                    0, 0)
-               : cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, true, false>, dummy, dummy, p, tiles_m,
-                                    tiles_n, 0, 0);
+               ? cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, true, true>, dummy, dummy, dummy, p, tiles_m,
+                                    tiles_n, 0, 0, 0)
+               : cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, true, false>, dummy, dummy, mc, p, tiles_m,
+                                    tiles_n, 0, 0, tma_store);
   }
-  EncodeFn enc = encode_fn();
-  if (!enc) return cudaErrorNotSupported;
   const CUtensorMapDataType dt = kTF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const int a_batched = (p.batch > 1 && p.sA != 0), b_batched = (p.batch > 1 && p.sB != 0);
   CUtensorMap ma, mb;
@@ -546,10 +616,10 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  return p.kslices > 1 ? cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, false, true>, ma, mb, p, tiles_m,
-                                            tiles_n, a_batched, b_batched)
-                      : cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, false, false>, ma, mb, p, tiles_m,
-                                           tiles_n, a_batched, b_batched);
+  return p.kslices > 1 ? cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, false, true>, ma, mb, mc, p,
+                                            tiles_m, tiles_n, a_batched, b_batched, 0)
+                      : cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, false, false>, ma, mb, mc, p,
+                                           tiles_m, tiles_n, a_batched, b_batched, tma_store);
 }
 
 // cudaOccupancyMaxActiveClusters of a (1, 1, slices) cluster launch (< 0: error).
