@@ -12,7 +12,7 @@ from paper_2008_13145_b200.dataset import KernelConfig  # noqa: E402
 
 CFGS = [(8, 1, 8, 16, 16), (8, 2, 8, 16, 16), (8, 4, 8, 16, 16), (8, 8, 8, 16, 16), (8, 4, 8, 8, 16),
         (8, 2, 8, 8, 16), (4, 8, 8, 16, 8), (8, 8, 4, 8, 16), (4, 2, 8, 16, 8), (4, 1, 2, 8, 8), (1, 1, 1, 8, 8),
-        (8, 4, 8, 16, 8), (8, 8, 4, 16, 16)]
+        (8, 4, 8, 16, 8), (8, 8, 4, 16, 16), (8, 8, 8, 16, 8)]
 SHAPES = [(8192, 8192, 8192), (4096, 4096, 4096), (12544, 4608, 512), (802816, 576, 64), (196, 4608, 512),
           (50176, 1152, 256)]
 dev = torch.device("cuda")

@@ -1,6 +1,7 @@
 """Small launches of every family / code path for compute-sanitizer (memcheck, racecheck,
 synccheck): F0 and F1 vector + scalar (unaligned) paths, tcgen05 TMA and LSU paths,
-epilogue bias/ReLU, im2col and max-pool."""
+k-sliced cluster launches (F1 and tcgen05: DSMEM slice reduction), the TMA-store
+epilogue, epilogue bias/ReLU, im2col and max-pool."""
 import sys
 
 import torch
@@ -20,6 +21,15 @@ for fam, cfg in cases:
         A = torch.rand(m, k, device=dev).to(dt)
         B = torch.rand(k, n, device=dev).to(dt)
         gemm.matmul(A, B, cfg, fam)
+# k-sliced launches (under-filled grid, long k): F1 float4 and scalar reduce paths, tcgen05
+for fam, cfg, (m, k, n) in (("simt", KernelConfig(4, 8, 8, 16, 8), (50, 2048, 70)),
+                            ("simt", KernelConfig(2, 1, 2, 64, 1), (33, 1100, 5)),
+                            ("bf16", gemm.family_configs("bf16")[1], (100, 3072, 200)),
+                            ("tf32", gemm.family_configs("tf32")[2], (64, 2001, 64))):
+    dt = gemm.input_dtype(fam)
+    from paper_2008_13145_b200.dataset import ProblemSize
+    assert gemm.k_slice_plan(cfg, ProblemSize(m, k, n, 1), family=fam)[0] > 1, (fam, cfg)
+    gemm.matmul(torch.rand(m, k, device=dev).to(dt), torch.rand(k, n, device=dev).to(dt), cfg, fam)
 lib = _lib.load()
 A = torch.rand(70, 64, device=dev)
 W = torch.rand(64, 72, device=dev)
