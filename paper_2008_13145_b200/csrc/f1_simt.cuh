@@ -166,8 +166,15 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
   // lane -> (row, col) inside the warp tile: adjacent lanes share the paired operand
   const int lr = Cfg::PAIR_B ? lane % Cfg::WTR : lane / Cfg::WTC;
   const int lc = Cfg::PAIR_B ? lane / Cfg::WTR : lane % Cfg::WTC;
-  const int ty = (warp / Cfg::WPC) * Cfg::WTR + lr;
-  const int tx = (warp % Cfg::WPC) * Cfg::WTC + lc;
+  // Warp-blocked ownership: warp (wy, wx) owns the contiguous R*WTR x C*WTC block at
+  // (wrow0, wcol0); inside it lane (lr, lc) takes rows wrow0 + r*WTR + lr and float-vector
+  // columns wcol0 + cv*WTC*VC + lc*VC.  Same shared-memory access pattern as a strided
+  // mapping (consecutive rows / consecutive vectors across the patch), but a tail tile's
+  // rows or columns beyond the problem land in whole warps, which then skip the math.
+  const int wrow0 = (warp / Cfg::WPC) * (R * Cfg::WTR);
+  const int wcol0 = (warp % Cfg::WPC) * (C * Cfg::WTC);
+  auto trow = [&](int r) { return wrow0 + r * Cfg::WTR + lr; };
+  auto tcol = [&](int cv) { return wcol0 + cv * Cfg::WTC * VC + lc * VC; };
 
   const int64_t gm = blockIdx.x / groups_n;
   const int gn = blockIdx.x - static_cast<int>(gm * groups_n);
@@ -175,6 +182,7 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
   const int m = p.m, k = p.k, n = p.n;
   const int64_t m0 = gm * BM;
   const int64_t n0 = static_cast<int64_t>(gn) * BN;
+  const bool warp_live = wrow0 < m - m0 && wcol0 < n - n0;
 
   const float* __restrict__ Ab = static_cast<const float*>(p.A) + b * p.sA;
   const float* __restrict__ Bb = static_cast<const float*>(p.B) + b * p.sB;
@@ -272,16 +280,17 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
     }
     const float* as = smem + (kt % STAGES) * Cfg::STAGE;
     const float* bs = as + BM * SA;
+    if (!warp_live) continue;  // this warp's whole block lies outside the problem
 #pragma unroll
     for (int kk = 0; kk < BK; kk += A) {
       float a[R][A];
 #pragma unroll
-      for (int r = 0; r < R; ++r) lds_vec<A>(as + (r * WGR + ty) * SA + kk, a[r]);
+      for (int r = 0; r < R; ++r) lds_vec<A>(as + trow(r) * SA + kk, a[r]);
 #pragma unroll
       for (int i = 0; i < A; ++i) {
         float w[C];
 #pragma unroll
-        for (int cv = 0; cv < C / VC; ++cv) lds_vec<VC>(bs + (kk + i) * SB + cv * WGC * VC + tx * VC, w + cv * VC);
+        for (int cv = 0; cv < C / VC; ++cv) lds_vec<VC>(bs + (kk + i) * SB + tcol(cv), w + cv * VC);
         if constexpr (C == 1) {
 #pragma unroll
           for (int r = 0; r < R; ++r) acc[r][0].x = __fmaf_rn(a[r][i], w[0], acc[r][0].x);
@@ -313,7 +322,7 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
           const float2 pr = acc[r][(cv * VC + e) / 2];
           v[e] = ((cv * VC + e) & 1) ? pr.y : pr.x;
         }
-        stg_vec<VC>(smem + (r * WGR + ty) * SP + cv * WGC * VC + tx * VC, v);
+        stg_vec<VC>(smem + trow(r) * SP + tcol(cv), v);
       }
     f1_slice_reduce<BM, BN, SP, NT>(p, smem, Cb, m0, n0);
     return;
@@ -321,12 +330,12 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
 
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int64_t row = m0 + r * WGR + ty;
+    const int64_t row = m0 + trow(r);
     if (row >= m) continue;
     float* out = Cb + row * p.ldc;
 #pragma unroll
     for (int cv = 0; cv < C / VC; ++cv) {
-      const int64_t col = n0 + cv * WGC * VC + tx * VC;
+      const int64_t col = n0 + tcol(cv);
       float v[VC];
 #pragma unroll
       for (int e = 0; e < VC; ++e) {

@@ -49,3 +49,28 @@ def test_dispatcher_matches_predict_tree_and_oracle(cuda_device):
         got = disp.matmul(torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)).cpu().numpy()
         _, kps = disp.k_slice_plan(p)
         assert np.array_equal(got.view(np.uint32), go.gemm_sliced(A, B, kps)[0].view(np.uint32))
+
+
+def test_bench_workload_full_size_bound(cuda_device):
+    """bench.py's workload at its full size (VGG16 GEMM layer set, batch 16, dispatched by
+    the committed B200 table's k-means 4 + treeA): every layer within the fp32 bound
+    |C - C64| <= 2*k*u*(|A||B|) of a float64 product -- the size-independent property the
+    bit-exact small-shape tests cannot cover at this scale (k-sliced layers included)."""
+    import bench
+    from paper_2008_13145_b200.dispatch import Dispatcher
+
+    pm, subset, tree, *_ = bench.train_selector(str(bench.DEFAULT_TABLE), 4, "kmeans", "treeA")
+    disp = Dispatcher(tree, subset, pm.configs, "simt")
+    g = torch.Generator(device=cuda_device).manual_seed(5)
+    sliced = 0
+    for name, p in dict(bench.vgg16_layers(16)).items():
+        A = torch.rand(p.m, p.k, device=cuda_device, generator=g) * 2 - 1
+        W = torch.rand(p.k, p.n, device=cuda_device, generator=g) * 2 - 1
+        C = disp.matmul(A, W).double()
+        A64, W64 = A.double(), W.double()
+        err = (C - A64 @ W64).abs()
+        bound = 2 * p.k * 2.0 ** -24 * (A64.abs() @ W64.abs())
+        assert bool((err <= bound).all()), name
+        sliced += disp.k_slice_plan(p)[0] > 1
+        del A, W, C, A64, W64, err, bound
+    assert sliced > 0  # the step exercises k-sliced launches
