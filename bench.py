@@ -112,34 +112,38 @@ class ClockSampler:
 
 
 def dist_setup(args):
+    """One process per GPU (torchrun env).  The process group pairs gloo for the host-side
+    timing collectives (max-over-ranks, barrier) with NCCL for device tensors; the data
+    path has no collective.  Returns (world, rank, device index)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 and args.impl == "ours":
-        import torch.distributed as dist
-        backend = "nccl" if args.impl == "ours" else "gloo"
-        if backend == "nccl":
-            import torch
-            torch.cuda.set_device(local)
-        dist.init_process_group(backend=backend)
+    if args.impl == "ours":
+        import torch
+        if torch.cuda.is_available():
+            local = local % torch.cuda.device_count()  # ranks > GPUs share (code-path tests only)
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group(backend="cpu:gloo,cuda:nccl")
     return world, rank, local
 
 
 def reduce_max(value: float, world: int, device=None) -> float:
-    """Max over ranks (the contract's multi-GPU timing rule)."""
+    """Max over ranks (the contract's multi-GPU timing rule), on the host group."""
     if world == 1:
         return value
     import torch
     import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device=device)
+    t = torch.tensor([value], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
 
 def barrier(world: int):
     if world > 1:
+        import torch
         import torch.distributed as dist
-        dist.barrier()
+        dist.all_reduce(torch.zeros(1), op=dist.ReduceOp.SUM)  # host-group barrier
 
 
 # ---------------------------------------------------------------- selection --
@@ -209,6 +213,7 @@ def cpu_baseline(batch: int = 1, repeats: int = 2):
 
     from oracle import gemm_oracle as go
 
+    threads = go.set_threads()  # all host CPUs, whatever OMP_NUM_THREADS the launcher set
     layers = vgg16_layers(batch)
     rng = np.random.default_rng(0)
     ops = [(rng.uniform(-1, 1, (p.m, p.k)).astype(np.float32), rng.uniform(-1, 1, (p.k, p.n)).astype(np.float32))
@@ -220,18 +225,40 @@ def cpu_baseline(batch: int = 1, repeats: int = 2):
         for A, B in ops:
             go.gemm_chain(A, B)
         best = min(best, time.perf_counter() - t0)
-    return flops / best / 1e9, best, flops
+    return flops / best / 1e9, best, flops, threads
+
+
+def cpu_blas_line(batch: int = 1, repeats: int = 2):
+    """Strongest CPU comparison: np.matmul fp32 (OpenBLAS, all host threads) on the same
+    bounded sample -- the reference package's numeric engine; reported
+    beside cpu_baseline, never a product path."""
+    import numpy as np
+
+    layers = vgg16_layers(batch)
+    rng = np.random.default_rng(0)
+    ops = [(rng.uniform(-1, 1, (p.m, p.k)).astype(np.float32), rng.uniform(-1, 1, (p.k, p.n)).astype(np.float32))
+           for _, p in layers]
+    flops = sum(p.flops for _, p in layers)
+    best = math.inf
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        for A, B in ops:
+            np.matmul(A, B)
+        best = min(best, time.perf_counter() - t0)
+    return {"value": flops / best / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "numpy-openblas",
+            "sample": f"VGG16 GEMM layer set at batch {batch} ({flops / 1e9:.2f} GFLOP, best of {repeats}), "
+                      "np.matmul fp32 (not the bit-exact fma chain)"}
 
 
 def run_reference(args, world, rank):
     """--impl reference: the CPU path (oracle port) on the host cores; rank 0 only."""
     if rank != 0:
         return 0
-    cores = os.cpu_count()
     sample_batch = 1
     gf, secs, flops = None, [], 0
     from oracle import gemm_oracle as go
     import numpy as np
+    cores = go.set_threads()  # torchrun exports OMP_NUM_THREADS=1; use every host CPU
     layers = vgg16_layers(sample_batch)
     rng = np.random.default_rng(0)
     ops = [(rng.uniform(-1, 1, (p.m, p.k)).astype(np.float32), rng.uniform(-1, 1, (p.k, p.n)).astype(np.float32))
@@ -389,12 +416,13 @@ def run_ours(args, world, rank, local):
         e2e = {"value": step_flops * args.steps * world / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps}
 
-    cpu = None
+    cpu = cpu_blas = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        gf, secs, flops = cpu_baseline(batch=1)
-        cpu = {"value": gf, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
+        gf, secs, flops, threads = cpu_baseline(batch=1)
+        cpu = {"value": gf, "unit": "GFLOP/s", "cores": threads, "kind": "port",
                "sample": f"VGG16 GEMM layer set at batch 1 ({flops / 1e9:.2f} GFLOP, best of 2) with "
                          f"oracle/gemm_ref.c (bit-exact fmaf chain, OpenMP all threads)"}
+        cpu_blas = cpu_blas_line(batch=1)
 
     if rank == 0:
         line = {
@@ -427,6 +455,7 @@ def run_ours(args, world, rank, local):
             line["e2e"] = e2e
         if cpu is not None:
             line["cpu_baseline"] = cpu
+            line["cpu_blas"] = cpu_blas
         print(json.dumps(line), flush=True)
     return 0
 

@@ -42,6 +42,8 @@ def lib():
         L.kp_ref_gemm_chain.argtypes = [i] * 4 + [vp, i64, i64, vp, i64, i64, vp, i64, i64]
         L.kp_ref_gemm_sliced.restype = None
         L.kp_ref_gemm_sliced.argtypes = [i] * 5 + [vp, i64, i64, vp, i64, i64, vp, i64, i64]
+        L.kp_ref_threads.restype = i
+        L.kp_ref_threads.argtypes = [i]
         L.kp_ref_gemm_f64.restype = None
         L.kp_ref_gemm_f64.argtypes = [i] * 4 + [vp, i64, i64, vp, i64, i64, vp, vp, i64, i64]
         _lib = L
@@ -59,6 +61,15 @@ def _batched(A: np.ndarray, B: np.ndarray):
     sA = m * k if A3.shape[0] > 1 else 0
     sB = k * n if B3.shape[0] > 1 else 0
     return A3, B3, batch, m, k, n, sA, sB
+
+
+def set_threads(n: int = 0) -> int:
+    """OpenMP threads for the oracle (n <= 0: all CPUs this process may run on);
+    returns the count in effect (torchrun exports OMP_NUM_THREADS=1 to each rank)."""
+    import os
+    if n <= 0:
+        n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    return int(lib().kp_ref_threads(int(n)))
 
 
 def gemm_tiled(A, B, config) -> tuple[np.ndarray, int]:

@@ -17,8 +17,16 @@
  * Build: make -C oracle   ->  oracle/libgemmref.so (OpenMP over work groups).
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <string.h>
+
+/* OpenMP team size for the oracle (n > 0 sets it; launchers such as torchrun export
+ * OMP_NUM_THREADS=1); returns the size now in effect. */
+int kp_ref_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+}
 
 /* Hardware FMA when the host has it (fmaf is correctly rounded either way, so the
  * clones are bit-identical); the default clone keeps the .so loadable anywhere. */
