@@ -184,22 +184,44 @@ __device__ __forceinline__ void lsu_stage(uint8_t* sa, uint8_t* sb, const GemmAr
   constexpr int ES = sizeof(Elem), BK = 128 / ES, NATOM = 128 / ES;
   const Elem* A = static_cast<const Elem*>(p.A) + static_cast<int64_t>(b) * p.sA;
   const Elem* B = static_cast<const Elem*>(p.B) + static_cast<int64_t>(b) * p.sB;
-  for (int e = t; e < BM * BK; e += 128) {
-    const int row = e / BK, kc = e - row * BK;
-    const int gr = m0 + row, gk = k0 + kc;
-    const Elem v = (gr < p.m && gk < p.k) ? A[static_cast<int64_t>(gr) * p.lda + gk] : Elem(0);
-    const int byte = kc * ES;
-    *reinterpret_cast<Elem*>(sa + (row >> 3) * 1024 + (row & 7) * 128 + (((byte >> 4) ^ (row & 7)) << 4) +
-                             (byte & 15)) = v;
+  // 8 independent loads in flight per thread before their shared-memory stores (a
+  // load-store-load chain leaves the 128 staging threads latency-bound)
+  constexpr int kBatch = 8;
+  static_assert((BM * BK / 128) % kBatch == 0 && (BK * BN / 128) % kBatch == 0, "LSU batches");
+#pragma unroll 1
+  for (int base = 0; base < BM * BK / 128; base += kBatch) {
+    Elem v[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int e = t + (base + j) * 128, row = e / BK, kc = e - row * BK;
+      const int gr = m0 + row, gk = k0 + kc;
+      v[j] = (gr < p.m && gk < p.k) ? A[static_cast<int64_t>(gr) * p.lda + gk] : Elem(0);
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int e = t + (base + j) * 128, row = e / BK, kc = e - row * BK;
+      const int byte = kc * ES;
+      *reinterpret_cast<Elem*>(sa + (row >> 3) * 1024 + (row & 7) * 128 + (((byte >> 4) ^ (row & 7)) << 4) +
+                               (byte & 15)) = v[j];
+    }
   }
-  for (int e = t; e < BK * BN; e += 128) {
-    const int kr = e / BN, nc = e - kr * BN;
-    const int gk = k0 + kr, gn = n0 + nc;
-    const Elem v = (gk < p.k && gn < p.n) ? B[static_cast<int64_t>(gk) * p.ldb + gn] : Elem(0);
-    const int j = nc / NATOM, byte = (nc - j * NATOM) * ES;
-    const int off = kTF32 ? (kr * 128 + (((byte >> 5) ^ (kr & 3)) << 5) + (byte & 31))  // 128B_BASE32B
-                          : ((kr >> 3) * 1024 + (kr & 7) * 128 + (((byte >> 4) ^ (kr & 7)) << 4) + (byte & 15));
-    *reinterpret_cast<Elem*>(sb + j * (BK * 128) + off) = v;
+#pragma unroll 1
+  for (int base = 0; base < BK * BN / 128; base += kBatch) {
+    Elem v[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int e = t + (base + j) * 128, kr = e / BN, nc = e - kr * BN;
+      const int gk = k0 + kr, gn = n0 + nc;
+      v[j] = (gk < p.k && gn < p.n) ? B[static_cast<int64_t>(gk) * p.ldb + gn] : Elem(0);
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int e = t + (base + j) * 128, kr = e / BN, nc = e - kr * BN;
+      const int jj = nc / NATOM, byte = (nc - jj * NATOM) * ES;
+      const int off = kTF32 ? (kr * 128 + (((byte >> 5) ^ (kr & 3)) << 5) + (byte & 31))  // 128B_BASE32B
+                            : ((kr >> 3) * 1024 + (kr & 7) * 128 + (((byte >> 4) ^ (kr & 7)) << 4) + (byte & 15));
+      *reinterpret_cast<Elem*>(sb + jj * (BK * 128) + off) = v[j];
+    }
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
