@@ -102,25 +102,24 @@ int kp_gemm_ex(int id, int m, int k, int n, int batch,
                const float* bias, int flags, void* stream);
 
 /* ---- k-slicing (SIMT, TF32 and BF16 families) ----------------------------
- * A launch whose output tiles cannot fill the GPU's resident-CTA slots (SIMT: SM count
- * x the config's occupancy target; tensor-core families: at most half the SMs get a
- * tile) cuts k into S <= 8 consecutive slices (SIMT launches of 1 to 3 waves with
- * k >= 512 use S = 2, which shrinks the partial last wave) (each at
- * least 256 (SIMT) / 768 (TF32, BF16) deep, aligned to the config's k-tile) computed by
- * the CTAs of one (1, 1, S) thread-block cluster per output tile (S is lowered until
- * cudaOccupancyMaxActiveClusters can co-schedule every tile's cluster in one wave on
- * the current device; the cap can be raised to the non-portable
- * cluster limit 16 with kp_set_max_k_slices); each output is then the fp32 fma chain
- * over every slice, summed in slice order ((p0 + p1) + p2) + ... through distributed
+ * A launch whose output tiles leave SMs idle or end in a partial wave cuts k into S
+ * consecutive slices, computed by the CTAs of one (1, 1, S) thread-block cluster per
+ * output tile and summed in slice order ((p0 + p1) + p2) + ... through distributed
  * shared memory -- deterministic for a given (config, shape, device).
+ *   SIMT:   u = output tiles / SMs; S = 8 (u < 0.5), 4 (u < 2), 2 (u < 6), else 1,
+ *           halved while the sliced grid exceeds 4 waves of resident CTAs, and never
+ *           shallower than 64 in k (a rule fitted on measured forced-S data).
+ *   TF32/BF16 (persistent 1-CTA/SM kernel): only grids filling at most half the SMs,
+ *           S = min(8, SMs / tiles, k / 768), lowered until every tile's cluster is
+ *           co-resident in one wave (cudaOccupancyMaxActiveClusters).
+ *   PAPER:  never (the paper's launch geometry).
  * kp_gemm_plan reports the plan kp_gemm would use: *k_slices = S and *k_per_slice =
  * the depth of every slice but the last (= k when S == 1).  num_sms <= 0 means the
- * current device's SM count and cluster limit (num_sms > 0 plans for a hypothetical
- * device with that many SMs and no cluster limit).  The PAPER family keeps the paper's
- * geometry and always reports S = 1.  kp_set_max_k_slices(1) disables slicing (every
- * SIMT output is then the single fma chain over k, bit-identical to the PAPER family,
- * and the tensor-core families run persistent); returns the previous setting
- * (default 8, range 1..16). */
+ * current device's SM count and cluster limits (num_sms > 0 plans for a hypothetical
+ * device with that many SMs and no cluster limit).  kp_set_max_k_slices caps S
+ * (1 disables slicing: every SIMT output is then the single fp32 fma chain over k,
+ * bit-identical to the PAPER family, and the tensor-core families run persistent);
+ * returns the previous cap (default 8, range 1..16). */
 int kp_set_max_k_slices(int max_slices);
 int kp_gemm_plan(int id, int m, int k, int n, int batch, int num_sms, int* k_slices, int* k_per_slice);
 

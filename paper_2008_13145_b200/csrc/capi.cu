@@ -110,7 +110,7 @@ int check_problem(int id, int m, int k, int n, int batch, const void* A, int64_t
 // a pure function of (config, shape, SM count), so results are deterministic on a
 // given GPU model and the oracle reproduces them from kp_gemm_plan.
 std::atomic<int> g_max_kslices{kp::kDefaultKSlices};
-constexpr int kMinSliceK = 256;    // never cut k into slices shallower than this (SIMT)
+constexpr int kMinSliceK = 64;     // never cut k into slices shallower than this (SIMT)
 constexpr int kMinSliceKTc = 768;  // tensor cores: shallower slices lose to the fixed costs
 
 int num_sms_current() {
@@ -180,20 +180,27 @@ void plan_slices(int id, int m, int k, int n, int batch, int sms, bool device, i
   int s = 1;
   if (slice_tile(v, &t) && max_slices > 1) {
     const int64_t tiles = ((m + t.bm - 1) / t.bm) * static_cast<int64_t>((n + t.bn - 1) / t.bn) * batch;
-    const int64_t slots = static_cast<int64_t>(sms) * t.occ;
-    const bool underfilled = v.family == KP_FAMILY_SIMT ? tiles < slots : 2 * tiles <= slots;
-    if (underfilled) {
-      const int64_t want = slots / tiles;
+    if (v.family == KP_FAMILY_SIMT) {
+      // Tiles per SM -> slices, fitted on 673 measured (shape, config) cells with every
+      // forced S (profiles/r1_kslicing.md): u < 0.5 -> 8, < 2 -> 4, < 6 -> 2, else 1;
+      // halved while the sliced grid would exceed 4 waves of resident CTAs, and never
+      // shallower than 64 in k.
+      const double u = static_cast<double>(tiles) / sms;
+      s = u < 0.5 ? 8 : u < 2.0 ? 4 : u < 6.0 ? 2 : 1;
+      while (s > 1 && tiles * s > 4LL * sms * t.occ) s /= 2;
+      if (s > max_slices) s = max_slices;
+      if (s > k / kMinSliceK) s = k / kMinSliceK;
+      if (s < 1) s = 1;
+      if (device && s > 1) s = fit_slices(id, v, s, 1);
+    } else if (2 * tiles <= static_cast<int64_t>(sms) * t.occ) {
+      // persistent tensor-core kernel: slice only grids that fill at most half the SMs,
+      // in one wave of clusters (a second wave of non-persistent CTAs loses to it)
+      const int64_t want = static_cast<int64_t>(sms) * t.occ / tiles;
       s = static_cast<int>(want < max_slices ? want : max_slices);
-      const int by_k = k / (v.family == KP_FAMILY_SIMT ? kMinSliceK : kMinSliceKTc);
+      const int by_k = k / kMinSliceKTc;
       if (s > by_k) s = by_k;
       if (s < 1) s = 1;
       if (device && s > 1) s = fit_slices(id, v, s, tiles);
-    } else if (v.family == KP_FAMILY_SIMT && tiles < 3 * slots && k >= 2 * kMinSliceK) {
-      // 1-3 waves: pairs of half-k CTAs shrink the partial last wave (measured +5-10 %
-      // at 1.3 and 2.7 waves, neutral beyond; tools/wave_probe.py)
-      s = max_slices < 2 ? max_slices : 2;
-      if (device && s > 1) s = fit_slices(id, v, s, 1);
     }
   }
   const int kt = (k + t.bk - 1) / t.bk;

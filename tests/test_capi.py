@@ -121,31 +121,29 @@ def test_dispatch_load_rejects_malformed_trees(lib):
 
 
 def test_k_slice_plan_host_logic(lib):
-    """kp_gemm_plan with an explicit SM count needs no GPU: slices only when the output
-    tiles cannot fill SMs x occupancy slots (or S = 2 at 1-3 waves), at most 8 by default,
-    never shallower than 256 in k,
-    no empty slice, k-tile aligned; other families and a cap of 1 never slice."""
+    """kp_gemm_plan with an explicit SM count needs no GPU.  SIMT rule (fitted on measured
+    forced-S data): tiles per SM u < 0.5 -> 8 slices, < 2 -> 4, < 6 -> 2, else 1,
+    halved while the grid would exceed 4 waves of resident CTAs, never shallower than 64
+    in k; no empty slice, k-tile aligned; the paper family and a cap of 1 never slice."""
     from paper_2008_13145_b200 import gemm
     probs = [ProblemSize(196, 4608, 512, 1), ProblemSize(32, 25088, 4096, 1), ProblemSize(1, 4096, 1000, 1),
              ProblemSize(12544, 4608, 512, 1), ProblemSize(3136, 2304, 256, 1), ProblemSize(50, 300, 70, 4),
-             ProblemSize(64, 255, 64, 1), ProblemSize(7, 100000, 9, 1)]
+             ProblemSize(64, 255, 64, 1), ProblemSize(7, 100000, 9, 1), ProblemSize(784, 512, 128, 1)]
     seen_sliced = 0
     for cfg in enumerate_configs()[::7]:
         tiles_m, tiles_n = cfg.tile_rows * cfg.wg_rows, cfg.tile_cols * cfg.wg_cols
         for p in probs:
             s, kps = gemm.k_slice_plan(cfg, p, num_sms=148)
-            assert 1 <= s <= 8
+            assert 1 <= s <= 8  # 8/4/2, fewer when k has fewer k-tiles than that
             if s == 1:
                 assert kps == p.k
                 continue
             seen_sliced += 1
-            assert p.k // s >= 128 and kps >= 256 // 2
+            assert p.k // s >= 64 and kps >= 64
             assert (s - 1) * kps < p.k <= s * kps  # no empty slice
             assert kps % 8 == 0  # a whole number of k-tiles (BK in {8, 16, 32})
             tiles = -(-p.m // tiles_m) * -(-p.n // tiles_n) * p.batch
-            assert tiles < 3 * 148 * 16  # under-filled (any S) or 1-3 waves (S = 2) only
-            if s > 2:
-                assert tiles < 148 * 16
+            assert tiles < (0.5 if s > 4 else 2 if s > 2 else 6) * 148  # tiles-per-SM bins
         big = ProblemSize(16384, 4096, 16384, 1)
         assert gemm.k_slice_plan(cfg, big, num_sms=148) == (1, 4096)
         assert gemm.k_slice_plan(cfg, ProblemSize(1, 4096, 1, 1), family="paper", num_sms=148) == (1, 4096)
