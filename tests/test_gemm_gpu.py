@@ -31,17 +31,41 @@ def _bits(x):
     return np.ascontiguousarray(x).view(np.uint32)
 
 
+def _want(A, B, cfg, family, cache):
+    """Oracle output for this launch: the single fma chain, or the sliced chain when the
+    SIMT planner k-slices it (kp_gemm_plan)."""
+    batch = max(A.shape[0], B.shape[0] if B.ndim == 3 else 1)
+    kps = gemm.k_slice_plan(cfg, dataset_problem((A.shape[1], A.shape[2], B.shape[-1], batch)), family)[1]
+    if kps not in cache:
+        cache[kps] = _bits(go.gemm_sliced(A, B, kps))
+    return cache[kps]
+
+
 @pytest.mark.parametrize("family", ["paper", "simt"])
 @pytest.mark.parametrize("shape", [(37, 27, 61, 3), (64, 128, 96, 1), (33, 147, 70, 2)])
 def test_all_640_configs_bit_exact(cuda_device, family, shape):
     A, B = _pair(*shape)
-    want = _bits(go.gemm_chain(A, B))
     dA, dB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
-    bad = []
+    cache, bad = {}, []
     for cfg in CONFIGS:
         got = gemm.matmul(dA, dB, cfg, family).cpu().numpy()
-        if not np.array_equal(_bits(got), want):
+        if not np.array_equal(_bits(got), _want(A, B, cfg, family, cache)):
             bad.append(cfg.as_tuple())
+    assert not bad, f"{len(bad)} configs differ, e.g. {bad[:5]}"
+
+
+@pytest.mark.parametrize("shape", [(64, 128, 96, 1), (33, 147, 70, 2)])
+def test_all_640_configs_single_chain_when_unsliced(cuda_device, shape):
+    """With k-slicing capped at 1 every SIMT config is the paper's single fp32 chain."""
+    A, B = _pair(*shape)
+    want = _bits(go.gemm_chain(A, B))
+    dA, dB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    prev = gemm.set_max_k_slices(1)
+    try:
+        bad = [cfg.as_tuple() for cfg in CONFIGS
+               if not np.array_equal(_bits(gemm.matmul(dA, dB, cfg, "simt").cpu().numpy()), want)]
+    finally:
+        gemm.set_max_k_slices(prev)
     assert not bad, f"{len(bad)} configs differ, e.g. {bad[:5]}"
 
 
@@ -52,19 +76,20 @@ EDGE = [1, 7, 31, 64, 255, 256, 1000]
 @pytest.mark.parametrize("m,k,n", [(m, k, n) for m in EDGE for k in (1, 31, 256) for n in (1, 64, 255)][::3])
 def test_edge_shapes_bit_exact(cuda_device, family, m, k, n):
     A, B = _pair(m, k, n, 1, seed=m + k + n)
-    want = _bits(go.gemm_chain(A, B))
     dA, dB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    cache = {}
     for cfg in (KernelConfig(8, 4, 8, 16, 16), KernelConfig(1, 1, 1, 1, 64), KernelConfig(4, 8, 2, 128, 1),
                 KernelConfig(2, 2, 8, 8, 32), KernelConfig(8, 1, 4, 64, 1)):
+        want = _want(A, B, cfg, family, cache)
         assert np.array_equal(_bits(gemm.matmul(dA, dB, cfg, family).cpu().numpy()), want), cfg
 
 
 @pytest.mark.parametrize("family", ["paper", "simt"])
 def test_broadcast_weights_and_strided_views(cuda_device, family):
     A, W = _pair(50, 72, 40, 4, seed=7, bcast=True)
-    want = _bits(go.gemm_chain(A, W))
-    dA, dW = torch.from_numpy(A).to(cuda_device), torch.from_numpy(W).to(cuda_device)
     cfg = KernelConfig(4, 4, 4, 16, 16)
+    want = _want(A, W, cfg, family, {})
+    dA, dW = torch.from_numpy(A).to(cuda_device), torch.from_numpy(W).to(cuda_device)
     assert np.array_equal(_bits(gemm.matmul(dA, dW, cfg, family).cpu().numpy()), want)
     # lda > k and ldb > n: operate on column slices of wider buffers
     big = torch.from_numpy(np.pad(A, ((0, 0), (0, 0), (0, 5)))).to(cuda_device)[:, :, :72]
