@@ -33,6 +33,49 @@ __global__ void im2col3x3_nhwc_kernel(const float* __restrict__ x, int B, int H,
   }
 }
 
+// Vectorised im2col for C % 4 == 0 (every VGG16 layer but conv1_1): one thread per
+// float4 of one tap of one output pixel, 32-bit index math (the 64-bit divisions of
+// the scalar kernel made it integer-bound, not HBM-bound).  Consecutive threads walk the
+// channels of a tap, then the taps, so loads and stores stay coalesced 16-byte accesses.
+__global__ void im2col3x3_nhwc_vec4_kernel(const float4* __restrict__ x, int B, int H, int W, int C4,
+                                           float4* __restrict__ out, int64_t ldo4, unsigned total) {
+  const unsigned K4 = 9u * C4;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned row = i / K4;
+    const unsigned kk = i - row * K4;
+    const unsigned tap = kk / C4, c4 = kk - tap * C4;
+    const int dy = static_cast<int>(tap / 3) - 1, dx = static_cast<int>(tap % 3) - 1;
+    const unsigned bh = row / W;
+    const int w = static_cast<int>(row - bh * W);
+    const unsigned b = bh / H;
+    const int h = static_cast<int>(bh - b * H);
+    const int hy = h + dy, wx = w + dx;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (hy >= 0 && hy < H && wx >= 0 && wx < W)
+      v = __ldg(x + ((static_cast<int64_t>(b) * H + hy) * W + wx) * C4 + c4);
+    out[static_cast<int64_t>(row) * ldo4 + kk] = v;
+  }
+}
+
+// 2x2 / stride 2 max pool, float4 over channels (C % 4 == 0), 32-bit index math.
+__global__ void maxpool2_nhwc_vec4_kernel(const float4* __restrict__ x, int B, int H, int W, int C4,
+                                          float4* __restrict__ out, unsigned total) {
+  const unsigned Ho = H / 2, Wo = W / 2;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned c4 = i % C4;
+    unsigned r = i / C4;
+    const unsigned wo = r % Wo;
+    r /= Wo;
+    const unsigned ho = r % Ho;
+    const unsigned b = r / Ho;
+    const float4* base = x + ((static_cast<int64_t>(b) * H + 2 * ho) * W + 2 * wo) * C4 + c4;
+    const float4 a0 = __ldg(base), a1 = __ldg(base + C4);
+    const float4 a2 = __ldg(base + static_cast<int64_t>(W) * C4), a3 = __ldg(base + static_cast<int64_t>(W) * C4 + C4);
+    out[i] = make_float4(fmaxf(fmaxf(a0.x, a1.x), fmaxf(a2.x, a3.x)), fmaxf(fmaxf(a0.y, a1.y), fmaxf(a2.y, a3.y)),
+                         fmaxf(fmaxf(a0.z, a1.z), fmaxf(a2.z, a3.z)), fmaxf(fmaxf(a0.w, a1.w), fmaxf(a2.w, a3.w)));
+  }
+}
+
 // 2x2 / stride 2 max pool; one thread per output element (channel fastest).
 __global__ void maxpool2_nhwc_kernel(const float* __restrict__ x, int B, int H, int W, int C, float* __restrict__ out) {
   const int Ho = H / 2, Wo = W / 2;
@@ -61,17 +104,31 @@ int grid_for(int64_t total, int threads) {
   return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 }  // namespace
 
 cudaError_t im2col3x3_nhwc_launch(const float* x, int B, int H, int W, int C, float* out, int64_t ldo,
                                   cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(B) * H * W * 9 * C;
+  if (C % 4 == 0 && ldo % 4 == 0 && aligned16(x) && aligned16(out) && total / 4 < 0x7fffffffLL) {
+    const unsigned t4 = static_cast<unsigned>(total / 4);
+    im2col3x3_nhwc_vec4_kernel<<<grid_for(t4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(x), B, H, W, C / 4,
+                                                                   reinterpret_cast<float4*>(out), ldo / 4, t4);
+    return cudaGetLastError();
+  }
   im2col3x3_nhwc_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, B, H, W, C, out, ldo);
   return cudaGetLastError();
 }
 
 cudaError_t maxpool2_nhwc_launch(const float* x, int B, int H, int W, int C, float* out, cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(B) * (H / 2) * (W / 2) * C;
+  if (C % 4 == 0 && aligned16(x) && aligned16(out) && total / 4 < 0x7fffffffLL) {
+    const unsigned t4 = static_cast<unsigned>(total / 4);
+    maxpool2_nhwc_vec4_kernel<<<grid_for(t4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(x), B, H, W, C / 4,
+                                                                  reinterpret_cast<float4*>(out), t4);
+    return cudaGetLastError();
+  }
   maxpool2_nhwc_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, B, H, W, C, out);
   return cudaGetLastError();
 }

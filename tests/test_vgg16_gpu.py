@@ -45,6 +45,26 @@ def test_im2col_and_pool_exact(cuda_device):
     assert np.array_equal(pout.cpu().numpy(), vgg16_ref.maxpool2(y))
 
 
+@pytest.mark.parametrize("B,H,W,C", [(2, 9, 7, 8), (3, 14, 14, 64), (1, 5, 6, 512)])
+def test_im2col_and_pool_vec4_exact(cuda_device, B, H, W, C):
+    """The float4 kernels (C % 4 == 0, every VGG16 layer after conv1_1), ldo > 9C too."""
+    lib = _lib.load()
+    rng = np.random.default_rng(C)
+    x = rng.standard_normal((B, H, W, C)).astype(np.float32)
+    dx = torch.from_numpy(x).to(cuda_device)
+    ldo = 9 * C + 4
+    out = torch.full((B * H * W, ldo), 7.0, device=cuda_device)
+    assert lib.kp_im2col3x3_nhwc(dx.data_ptr(), B, H, W, C, out.data_ptr(), ldo, None) == 0
+    assert np.array_equal(out[:, :9 * C].cpu().numpy(), vgg16_ref.im2col3x3(x))
+    assert bool((out[:, 9 * C:] == 7.0).all())
+    H2, W2 = H - H % 2, W - W % 2
+    y = np.ascontiguousarray(x[:, :H2, :W2, :])
+    dy = torch.from_numpy(y).to(cuda_device)
+    pout = torch.empty(B, H2 // 2, W2 // 2, C, device=cuda_device)
+    assert lib.kp_maxpool2x2_nhwc(dy.data_ptr(), B, H2, W2, C, pout.data_ptr(), None) == 0
+    assert np.array_equal(pout.cpu().numpy(), vgg16_ref.maxpool2(y))
+
+
 @pytest.mark.parametrize("batch", [1, 2])
 def test_vgg16_forward_bit_exact(cuda_device, batch):
     convs, fcs = vgg16.init_weights(seed=0)
