@@ -80,3 +80,27 @@ def test_vgg16_forward_bit_exact(cuda_device, batch):
     again = model.forward(x.to(cuda_device)).cpu().numpy()
     torch.cuda.synchronize()
     assert np.array_equal(again.view(np.uint32), want.view(np.uint32))
+
+
+def test_vgg16_forward_tf32_family_within_tolerance(cuda_device):
+    """VGG16 inference on the tcgen05 TF32 family (fp32 activations, tf32 products, fp32
+    accumulation): logits within a stated normwise tolerance of the bit-exact fp32 oracle
+    forward -- 16 layers of TF32 products (2^-11 relative operand rounding each, ReLU
+    between) stay below 2e-2 relative in the 2-norm."""
+    from paper_2008_13145_b200 import gemm
+    from paper_2008_13145_b200.classify import TreeModel
+    from paper_2008_13145_b200.selection import ConfigSubset
+
+    cfgs = gemm.family_configs("tf32")
+    leaf = TreeModel(feature=np.array([-1]), threshold=np.array([np.nan]), left=np.array([-1]),
+                     right=np.array([-1]), leaf_class=np.array([0]))
+    disp = Dispatcher(leaf, ConfigSubset((3,), "fixed", 1, 1), cfgs, "tf32")  # (128,32,256,4,192)
+    convs, fcs = vgg16.init_weights(seed=0)
+    model = vgg16.Vgg16(disp, 1, cuda_device, weights=(convs, fcs))
+    x = torch.randn(1, 224, 224, 3, generator=torch.Generator().manual_seed(7))
+    got = model.forward(x.to(cuda_device)).double().cpu().numpy()
+    want = vgg16_ref.forward(x.numpy(), [(w.numpy(), b.numpy()) for w, b in convs],
+                             [(w.numpy(), b.numpy()) for w, b in fcs]).astype(np.float64)
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert rel < 2e-2, rel
+    assert not np.array_equal(got, want)  # it really ran on the tensor cores

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out/job42
+for B in 1 16 64; do
+  timeout 900 python bench.py --workload vgg16-infer --family tf32 --table data/sweeps/vgg16_tf32.csv --batch $B --steps 20 > gpurun_out/job42/vgg16_tf32_b$B.json 2> gpurun_out/job42/vgg16_tf32_b$B.err; echo "rc=$?"; tail -c 200 gpurun_out/job42/vgg16_tf32_b$B.json; tail -3 gpurun_out/job42/vgg16_tf32_b$B.err
+done
