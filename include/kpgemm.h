@@ -109,9 +109,13 @@ int kp_gemm_ex(int id, int m, int k, int n, int batch,
  *   SIMT:   u = output tiles / SMs; S = 8 (u < 0.5), 4 (u < 2), 2 (u < 6), else 1,
  *           halved while the sliced grid exceeds 4 waves of resident CTAs, and never
  *           shallower than 64 in k (a rule fitted on measured forced-S data).
- *   TF32/BF16 (persistent 1-CTA/SM kernel): only grids filling at most half the SMs,
+ *   TF32/BF16 (persistent 1-CTA/SM kernel): grids filling at most half the SMs,
  *           S = min(8, SMs / tiles, k / 768), lowered until every tile's cluster is
- *           co-resident in one wave (cudaOccupancyMaxActiveClusters).
+ *           co-resident in one wave (cudaOccupancyMaxActiveClusters); and for grids of
+ *           more than one wave with long tiles (BN*k >= 1.72e6, TF32 0.86e6) whose
+ *           partial last wave fills at most half the SMs, those tail tiles only, as a
+ *           second sliced launch after the persistent one (kp_gemm_plan then reports
+ *           the tail launch's S and depth).
  *   PAPER:  never (the paper's launch geometry).
  * kp_gemm_plan reports the plan kp_gemm would use: *k_slices = S and *k_per_slice =
  * the depth of every slice but the last (= k when S == 1).  num_sms <= 0 means the

@@ -172,8 +172,12 @@ int fit_slices(int id, const Variant& v, int want, int64_t clusters) {
 // The k-slice plan of variant id on (m, k, n, batch): S slices of kt_per_slice k-tiles
 // (S == 1: kt_per_slice = all k-tiles).  sms > 0 with device == false plans for a
 // hypothetical device (no cluster-occupancy query).
+struct TailPlan {
+  int tail_tiles = 0, tail_slices = 0, kt_per_slice_tail = 0;
+};
+
 void plan_slices(int id, int m, int k, int n, int batch, int sms, bool device, int* slices, int* kt_per_slice,
-                 int* bk) {
+                 int* bk, TailPlan* tail_out = nullptr) {
   const Variant& v = registry().variants[id];
   SliceTile t{1, 1, k, 1};
   const int max_slices = g_max_kslices.load(std::memory_order_relaxed);
@@ -201,6 +205,25 @@ void plan_slices(int id, int m, int k, int n, int batch, int sms, bool device, i
       if (s > by_k) s = by_k;
       if (s < 1) s = 1;
       if (device && s > 1) s = fit_slices(id, v, s, tiles);
+    } else if (tail_out && tiles > sms) {
+      // more than one wave: the persistent kernel keeps the full waves; a partial last
+      // wave filling at most half the SMs runs as a separate k-sliced launch
+      // Only for long tiles (>= ~40 us of MMA: BN*k >= 1.72e6 for BF16, half that for TF32
+      // at half the rate): the second launch, its pipeline fill and the DSMEM reduction
+      // cost ~10 us, so shorter tails measured slower (profiles/r1_tc_epilogue.md).
+      const int64_t r = tiles % sms;
+      const int64_t work = static_cast<int64_t>(t.bn) * k * (v.family == KP_FAMILY_TF32 ? 2 : 1);
+      if (r > 0 && 2 * r <= sms && k >= 2 * kMinSliceKTc && work >= 1720000) {
+        int ts = static_cast<int>(sms / r < max_slices ? sms / r : max_slices);
+        if (ts > k / kMinSliceKTc) ts = k / kMinSliceKTc;
+        if (device && ts > 1) ts = fit_slices(id, v, ts, r);
+        if (ts > 1) {
+          const int kt = (k + t.bk - 1) / t.bk;
+          tail_out->tail_tiles = static_cast<int>(r);
+          tail_out->tail_slices = ts;
+          tail_out->kt_per_slice_tail = (kt + ts - 1) / ts;
+        }
+      }
     }
   }
   const int kt = (k + t.bk - 1) / t.bk;
@@ -231,7 +254,10 @@ int launch(int id, const kp::GemmArgs& p0, cudaStream_t s) {
         const int sms = num_sms_current();
         if (sms < 1) return fail(KP_EIO, "cannot query the SM count of the current device");
         int bk = 0;
-        plan_slices(id, p.m, p.k, p.n, p.batch, sms, true, &p.kslices, &p.kt_per_slice, &bk);
+        TailPlan tail;
+        plan_slices(id, p.m, p.k, p.n, p.batch, sms, true, &p.kslices, &p.kt_per_slice, &bk, &tail);
+        p.tail_tiles = tail.tail_tiles;
+        p.tail_slices = tail.tail_slices;
         static const int forced = [] {  // dev-only override for planner experiments
           const char* e = std::getenv("KPGEMM_FORCE_SLICES");
           return e ? std::atoi(e) : 0;
@@ -260,6 +286,7 @@ kp::GemmArgs make_args(int m, int k, int n, int batch, const void* A, int64_t ld
   p.a_vec = p.b_vec = p.c_vec = p.c_vec4 = 0;
   p.kslices = 1;
   p.kt_per_slice = 0;
+  p.tail_tiles = p.tail_slices = 0;
   p.bias = nullptr;
   p.relu = 0;
   return p;
@@ -368,7 +395,13 @@ int kp_gemm_plan(int id, int m, int k, int n, int batch, int num_sms, int* k_sli
     if (num_sms < 1) return fail(KP_EIO, "cannot query the SM count of the current device");
   }
   int s = 1, per = 0, bk = 1;
-  plan_slices(id, m, k, n, batch, num_sms > 0 ? num_sms : 1, device, &s, &per, &bk);
+  TailPlan tail;
+  plan_slices(id, m, k, n, batch, num_sms > 0 ? num_sms : 1, device, &s, &per, &bk, &tail);
+  if (s == 1 && tail.tail_slices > 1) {  // tensor cores: the partial last wave's launch
+    const int kt = (k + bk - 1) / bk;
+    per = tail.kt_per_slice_tail;
+    s = (kt + per - 1) / per;
+  }
   *k_slices = s;
   const int64_t depth = static_cast<int64_t>(per) * bk;
   *k_per_slice = s == 1 ? k : static_cast<int>(depth < k ? depth : k);

@@ -33,6 +33,10 @@ struct GemmArgs {
   // plain single-chain kernel.
   int kslices;
   int kt_per_slice;
+  // Tensor-core families only: the last tail_tiles output tiles (a partial last wave of
+  // the persistent kernel) run as a second, k-sliced launch with tail_slices slices.
+  int tail_tiles;
+  int tail_slices;
 };
 
 // Epilogue of every family: bias add (fp32, round-to-nearest) then ReLU.  Applied

@@ -248,12 +248,13 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 // over every rank's shared-memory partial (DSMEM) in rank order, then applies the
 // epilogue and stores.  Same slice order as the SIMT family: ((p0 + p1) + p2) + ...
 template <int BN>
-__device__ __forceinline__ void tc_slice_reduce(const GemmArgs& p, float* part, int tiles_m, int tiles_n) {
+__device__ __forceinline__ void tc_slice_reduce(const GemmArgs& p, float* part, int tiles_m, int tiles_n,
+                                                int tile_begin) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   cl.sync();
   int b, m0, n0;
-  tile_coords<BN>(blockIdx.x, tiles_m, tiles_n, b, m0, n0);
+  tile_coords<BN>(tile_begin + static_cast<int>(blockIdx.x), tiles_m, tiles_n, b, m0, n0);
   constexpr int PS = BN + 4, Q = BN / 4, TOT = BM * Q;
   const int S = p.kslices, z = static_cast<int>(cl.block_rank());
   const int chunk = (TOT + S - 1) / S, end = min(TOT, (z + 1) * chunk);
@@ -293,7 +294,7 @@ template <bool kTF32, int BN, int STAGES, bool kLsu, bool kSliced>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapC, GemmArgs p, int tiles_m, int tiles_n, int a_batched,
-                   int b_batched, int tma_store) {
+                   int b_batched, int tma_store, int tile_begin, int tile_count) {
   using Cfg = TcCfg<kTF32, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -310,7 +311,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int KT = kSliced ? min((p.k + Cfg::BK - 1) / Cfg::BK - kt0, p.kt_per_slice) : (p.k + Cfg::BK - 1) / Cfg::BK;
   constexpr bool sliced = kSliced;
   const int per_batch = tiles_m * tiles_n;
-  const int n_tiles = per_batch * p.batch;
+  const int n_tiles = tile_count;  // this launch's tiles: [tile_begin, tile_begin + tile_count)
+  (void)per_batch;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -342,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0;  // global k-iteration counter (ring position across tiles)
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       int b, m0, n0;
-      tile_coords<BN>(t, tiles_m, tiles_n, b, m0, n0);
+      tile_coords<BN>(tile_begin + t, tiles_m, tiles_n, b, m0, n0);
       const int za = a_batched ? b : 0, zb = b_batched ? b : 0;
       for (int kt = 0; kt < KT; ++kt, ++it) {
         const int s = it % STAGES;
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0, i = 0, epi_box = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
       int b, m0, n0;
-      tile_coords<BN>(t, tiles_m, tiles_n, b, m0, n0);
+      tile_coords<BN>(tile_begin + t, tiles_m, tiles_n, b, m0, n0);
       if constexpr (kLsu) {
         const int tid = threadIdx.x - 64;
         for (int kt = 0; kt < KT; ++kt, ++it) {
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
   }
-  if constexpr (sliced) tc_slice_reduce<BN>(p, reinterpret_cast<float*>(smem), tiles_m, tiles_n);
+  if constexpr (sliced) tc_slice_reduce<BN>(p, reinterpret_cast<float*>(smem), tiles_m, tiles_n, tile_begin);
 }
 
 // ---------------------------------------------------------------- host side --
@@ -565,20 +567,13 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   } else if (p.kslices > kMaxKSlices || n_tiles * p.kslices > 0x7fffffffLL) {
     return cudaErrorInvalidConfiguration;  // sliced launches run one (tile, slice) per CTA
   }
-  // k-sliced: grid (#tiles, 1, S) in (1, 1, S) clusters; else persistent over the SMs
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = p.kslices > 1 ? dim3(static_cast<unsigned>(n_tiles), 1, p.kslices)
-                             : dim3(static_cast<unsigned>(n_tiles < num_sms() ? n_tiles : num_sms()));
-  lc.blockDim = dim3(kThreads);
-  lc.dynamicSmemBytes = p.kslices > 1 ? Cfg::SLICED_SMEM_BYTES : Cfg::SMEM_BYTES;
-  lc.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 1;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = p.kslices;
-  lc.attrs = at;
-  lc.numAttrs = p.kslices > 1 ? 1 : 0;
+  // tail split (planner, capi.cu): the last tail_tiles tiles run as a second, sliced launch
+  int tail = 0, tail_s = 1;
+  if (p.kslices == 1 && p.tail_slices > 1 && p.tail_tiles > 0 && p.tail_tiles < n_tiles &&
+      p.tail_slices <= kMaxKSlices) {
+    tail = p.tail_tiles;
+    tail_s = p.tail_slices;
+  }
   EncodeFn enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
   // C as a TMA store target: persistent launches with 16-byte-aligned C rows and a short
@@ -600,48 +595,83 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
-  if (!tma_ok(p, Cfg::ES)) {
-    CUtensorMap dummy;
-    std::memset(&dummy, 0, sizeof(dummy));
-    return p.kslices > 1
-               ? cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, true, true>, dummy, dummy, dummy, p, tiles_m,
-                                    tiles_n, 0, 0, 0)
-               : cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, true, false>, dummy, dummy, mc, p, tiles_m,
-                                    tiles_n, 0, 0, tma_store);
-  }
-  const CUtensorMapDataType dt = kTF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const bool lsu = !tma_ok(p, Cfg::ES);
   const int a_batched = (p.batch > 1 && p.sA != 0), b_batched = (p.batch > 1 && p.sB != 0);
   CUtensorMap ma, mb;
-  {
-    cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.k), static_cast<cuuint64_t>(p.m),
-                          static_cast<cuuint64_t>(a_batched ? p.batch : 1)};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.lda) * Cfg::ES,
-                             static_cast<cuuint64_t>(a_batched ? p.sA : p.lda * p.m) * Cfg::ES};
-    if (!a_batched) strides[1] = (strides[1] + 15) / 16 * 16;
-    cuuint32_t box[3] = {static_cast<cuuint32_t>(Cfg::BK), static_cast<cuuint32_t>(BM), 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    if (enc(&ma, dt, 3, const_cast<void*>(p.A), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return cudaErrorInvalidValue;
+  std::memset(&ma, 0, sizeof(ma));
+  std::memset(&mb, 0, sizeof(mb));
+  if (!lsu) {
+    const CUtensorMapDataType dt = kTF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    {
+      cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.k), static_cast<cuuint64_t>(p.m),
+                            static_cast<cuuint64_t>(a_batched ? p.batch : 1)};
+      cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.lda) * Cfg::ES,
+                               static_cast<cuuint64_t>(a_batched ? p.sA : p.lda * p.m) * Cfg::ES};
+      if (!a_batched) strides[1] = (strides[1] + 15) / 16 * 16;
+      cuuint32_t box[3] = {static_cast<cuuint32_t>(Cfg::BK), static_cast<cuuint32_t>(BM), 1};
+      cuuint32_t es[3] = {1, 1, 1};
+      if (enc(&ma, dt, 3, const_cast<void*>(p.A), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
+    {
+      cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.n), static_cast<cuuint64_t>(p.k),
+                            static_cast<cuuint64_t>(b_batched ? p.batch : 1)};
+      cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.ldb) * Cfg::ES,
+                               static_cast<cuuint64_t>(b_batched ? p.sB : p.ldb * p.k) * Cfg::ES};
+      if (!b_batched) strides[1] = (strides[1] + 15) / 16 * 16;
+      cuuint32_t box[3] = {static_cast<cuuint32_t>(Cfg::NATOM), static_cast<cuuint32_t>(Cfg::BK), 1};
+      cuuint32_t es[3] = {1, 1, 1};
+      if (enc(&mb, dt, 3, const_cast<void*>(p.B), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              kTF32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
   }
-  {
-    cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.n), static_cast<cuuint64_t>(p.k),
-                          static_cast<cuuint64_t>(b_batched ? p.batch : 1)};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.ldb) * Cfg::ES,
-                             static_cast<cuuint64_t>(b_batched ? p.sB : p.ldb * p.k) * Cfg::ES};
-    if (!b_batched) strides[1] = (strides[1] + 15) / 16 * 16;
-    cuuint32_t box[3] = {static_cast<cuuint32_t>(Cfg::NATOM), static_cast<cuuint32_t>(Cfg::BK), 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    if (enc(&mb, dt, 3, const_cast<void*>(p.B), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            kTF32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return cudaErrorInvalidValue;
+  // one launch over tiles [t0, t0 + count): persistent (slices == 1, grid <= SMs) or
+  // k-sliced (grid (count, 1, slices) in (1, 1, slices) clusters)
+  auto go = [&](GemmArgs q, int t0, int count, int slices) -> cudaError_t {
+    if (slices > 1) {  // no empty slice: every CTA must accumulate at least one k-tile
+      const int per = (KT + slices - 1) / slices;
+      slices = (KT + per - 1) / per;
+    }
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = slices;
+    lc.gridDim = slices > 1 ? dim3(static_cast<unsigned>(count), 1, slices)
+                            : dim3(static_cast<unsigned>(count < num_sms() ? count : num_sms()));
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = slices > 1 ? Cfg::SLICED_SMEM_BYTES : Cfg::SMEM_BYTES;
+    lc.stream = s;
+    lc.attrs = at;
+    lc.numAttrs = slices > 1 ? 1 : 0;
+    if (slices > 1) {
+      q.kslices = slices;
+      q.kt_per_slice = (KT + slices - 1) / slices;
+      return lsu ? cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, true, true>, ma, mb, mc, q, tiles_m,
+                                      tiles_n, 0, 0, 0, t0, count)
+                 : cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, false, true>, ma, mb, mc, q, tiles_m,
+                                      tiles_n, a_batched, b_batched, 0, t0, count);
+    }
+    q.kslices = 1;
+    q.kt_per_slice = KT;
+    return lsu ? cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, true, false>, ma, mb, mc, q, tiles_m,
+                                    tiles_n, 0, 0, tma_store, t0, count)
+               : cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, false, false>, ma, mb, mc, q, tiles_m,
+                                    tiles_n, a_batched, b_batched, tma_store, t0, count);
+  };
+  const int total = static_cast<int>(n_tiles);
+  if (p.kslices > 1) return go(p, 0, total, p.kslices);  // the whole grid sliced
+  if (tail > 0) {
+    cudaError_t e = go(p, 0, total - tail, 1);
+    if (e != cudaSuccess) return e;
+    return go(p, total - tail, tail, tail_s);
   }
-  return p.kslices > 1 ? cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, false, true>, ma, mb, mc, p,
-                                            tiles_m, tiles_n, a_batched, b_batched, 0)
-                      : cudaLaunchKernelEx(&lc, tc_gemm_kernel<kTF32, BN, STAGES, false, false>, ma, mb, mc, p,
-                                           tiles_m, tiles_n, a_batched, b_batched, tma_store);
+  return go(p, 0, total, 1);
 }
 
 // cudaOccupancyMaxActiveClusters of a (1, 1, slices) cluster launch (< 0: error).

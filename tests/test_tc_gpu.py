@@ -107,3 +107,22 @@ def test_k_sliced_epilogue(cuda_device, fam):
                                       bias.data_ptr(), _lib.KP_EPI_RELU, torch.cuda.current_stream().cuda_stream),
                "kp_gemm_ex")
     assert torch.equal(C, torch.relu(plain + bias))
+
+
+@pytest.mark.parametrize("fam,m,k,n,batch", [("tf32", 2560, 4096, 4096, 1), ("bf16", 2560, 8192, 4096, 1),
+                                              ("tf32", 640, 4096, 4096, 4)])
+def test_partial_last_wave_split(cuda_device, fam, m, k, n, batch):
+    """Grids of more than one wave whose last wave fills at most half the SMs run the tail
+    tiles as a second, k-sliced launch: every config within the bound, deterministic."""
+    from paper_2008_13145_b200.dataset import ProblemSize
+    split = 0
+    for cfg in gemm.family_configs(fam):
+        split += gemm.k_slice_plan(cfg, ProblemSize(m, k, n, batch), family=fam)[0] > 1
+        _check(fam, cfg, m, k, n, batch, cuda_device, bcast=(batch > 1), seed=n)
+    assert split > 0
+    g = torch.Generator(device=cuda_device).manual_seed(2)
+    dt = torch.bfloat16 if fam == "bf16" else torch.float32
+    A = (torch.rand(m, k, device=cuda_device, generator=g) - 0.5).to(dt)
+    B = (torch.rand(k, n, device=cuda_device, generator=g) - 0.5).to(dt)
+    cfg = gemm.family_configs(fam)[2]
+    assert torch.equal(gemm.matmul(A, B, cfg, fam), gemm.matmul(A, B, cfg, fam))

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out/job45
+timeout 900 python -m pytest tests/test_tc_gpu.py -q -x > gpurun_out/job45/pytest.log 2>&1; tail -3 gpurun_out/job45/pytest.log
+timeout 600 python tools/tc_ab.py 8 > gpurun_out/job45/new.json 2>&1

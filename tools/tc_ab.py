@@ -15,7 +15,8 @@ lib = _lib.load()
 if hasattr(lib, "kp_set_max_k_slices"):
     lib.kp_set_max_k_slices(cap)
 SHAPES = [(3211264, 27, 64), (100352, 147, 64), (12544, 4608, 512), (6272, 1152, 256), (784, 512, 256),
-          (3136, 576, 64), (1568, 4608, 512), (8192, 8192, 8192), (16384, 64, 16384), (16384, 16384, 64)]
+          (3136, 576, 64), (1568, 4608, 512), (8192, 8192, 8192), (16384, 64, 16384), (16384, 16384, 64), (4096, 4096, 4096),
+          (2560, 4096, 4096), (12544, 2304, 512)]
 dev = torch.device("cuda")
 res = {}
 for fam in ("bf16", "tf32"):
