@@ -103,12 +103,12 @@ int check_problem(int id, int m, int k, int n, int batch, const void* A, int64_t
 }
 
 // ------------------------------------------------------------- k-slicing --
-// When a SIMT launch has fewer output tiles than the GPU has resident-CTA slots
-// (mid-size m x n with a long k: VGG16 conv5 / fc at small batch), the k-tiles are
+// When a launch's output tiles leave SMs idle or end in a partial wave, the k-tiles are
 // cut into S consecutive slices computed by the S CTAs of a (1, 1, S) cluster and
-// summed in slice order through distributed shared memory (f1_simt.cuh).  The plan is
-// a pure function of (config, shape, SM count), so results are deterministic on a
-// given GPU model and the oracle reproduces them from kp_gemm_plan.
+// summed in slice order through distributed shared memory (f1_simt.cuh, tc_gemm.cu);
+// plan_slices below holds the rules (include/kpgemm.h documents them).  The plan is a
+// pure function of (config, shape, device), so results are deterministic on a given GPU
+// model and the oracle reproduces the SIMT ones from kp_gemm_plan.
 std::atomic<int> g_max_kslices{kp::kDefaultKSlices};
 constexpr int kMinSliceK = 64;     // never cut k into slices shallower than this (SIMT)
 constexpr int kMinSliceKTc = 768;  // tensor cores: shallower slices lose to the fixed costs
