@@ -37,7 +37,11 @@ from .dataset import (KernelConfig, PerfMatrix, ProblemSize, SynthModel, seriali
                       synth_generate)
 from .errors import DataError
 
-SIDECAR_HEADER = "m,k,n,batch,config_index,mean_ms,iters,gflops"
+# Per-cell record of a sweep shard (the partial / resume file).  sm_mhz and temp_c are
+# the SM clock and GPU temperature sampled right after the cell's timed loop (NVML;
+# empty for timers without a device), the SURVEY 8(d) per-cell conditions record.
+SIDECAR_HEADER = "m,k,n,batch,config_index,mean_ms,iters,gflops,sm_mhz,temp_c"
+_OLD_SIDECAR_HEADER = "m,k,n,batch,config_index,mean_ms,iters,gflops"
 
 
 class Timer(Protocol):
@@ -97,6 +101,29 @@ class CudaEventTimer:
         self.stream = torch.cuda.Stream(self.device)
         self._ops_key = None
         self._ops = None
+        self._nvml = None
+
+    def conditions(self) -> tuple[str, str]:
+        """(SM clock MHz, temperature C) of this timer's GPU now, via NVML ('' if absent)."""
+        if self._nvml is None:
+            try:
+                import pynvml
+                pynvml.nvmlInit()
+                idx = self.device.index or 0
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+                if vis and all(v.strip().isdigit() for v in vis.split(",")):
+                    idx = int(vis.split(",")[idx])  # NVML numbers physical GPUs
+                self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx))
+            except Exception:
+                self._nvml = False
+        if not self._nvml:
+            return "", ""
+        nv, h = self._nvml
+        try:
+            return (str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                    str(nv.nvmlDeviceGetTemperature(h, nv.NVML_TEMPERATURE_GPU)))
+        except Exception:
+            return "", ""
 
     def operands(self, problem: ProblemSize):
         if self._ops_key != problem:
@@ -143,10 +170,11 @@ def _read_partial(path: Path) -> dict[tuple[ProblemSize, int], tuple[float, floa
     with path.open() as fh:
         reader = csv.reader(fh)
         header = next(reader, None)
-        if header is None or ",".join(header) != SIDECAR_HEADER:
+        if header is None or ",".join(header) not in (SIDECAR_HEADER, _OLD_SIDECAR_HEADER):
             raise DataError(f"{path}: not a sweep partial file")
+        width = len(header)
         for row in reader:
-            if len(row) != 8:
+            if len(row) != width:
                 continue  # torn last line of an interrupted run
             m, k, n, b, ci = (int(v) for v in row[:5])
             done[(ProblemSize(m, k, n, b), ci)] = (float(row[7]), float(row[5]), int(row[6]))
@@ -180,7 +208,9 @@ def run_shard(problems, rows: Iterable[int], n_configs: int, timer: Timer, parti
                     raise DataError(f"failed measurement for {p} / config {ci}")
                 out[(p, ci)] = (g, ms, iters)
                 if fh is not None:
-                    fh.write(f"{p.m},{p.k},{p.n},{p.batch},{ci},{ms!r},{iters},{g!r}\n")
+                    cond = getattr(timer, "conditions", None)
+                    mhz, temp = cond() if cond is not None else ("", "")
+                    fh.write(f"{p.m},{p.k},{p.n},{p.batch},{ci},{ms!r},{iters},{g!r},{mhz},{temp}\n")
                 if progress is not None:
                     progress(count, total)
     finally:
