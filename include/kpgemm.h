@@ -179,6 +179,11 @@ int kp_gemm_auto_ex(int handle, int m, int k, int n, int batch,
  * r = (b*H + h)*W + w holds the 9*C patch values ordered (dy, dx, c) -- the k order of
  * the (9*C) x Cout weight matrix -- with zeros outside the image; ldo >= 9*C. */
 int kp_im2col3x3_nhwc(const float* x, int B, int H, int W, int C, float* out, int64_t ldo, void* stream);
+/* Same patches into rows of kpad >= 9*C floats (kpad % 4 == 0, out 16-byte aligned),
+ * zeros in columns 9*C..kpad-1: e.g. conv1_1 (C = 3) as 28-wide rows, which the GEMM
+ * families read with their vector / TMA paths (pair it with a zero-padded weight row:
+ * fma(0, 0, acc) == acc, so the fp32 chain is unchanged). */
+int kp_im2col3x3_nhwc_pad(const float* x, int B, int H, int W, int C, float* out, int kpad, void* stream);
 /* 2x2 / stride 2 max pooling, NHWC: (B, H, W, C) -> (B, H/2, W/2, C). */
 int kp_maxpool2x2_nhwc(const float* x, int B, int H, int W, int C, float* out, void* stream);
 

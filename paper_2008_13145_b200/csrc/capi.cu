@@ -498,6 +498,15 @@ int kp_im2col3x3_nhwc(const float* x, int B, int H, int W, int C, float* out, in
   return e == cudaSuccess ? KP_OK : cuda_fail(e, "im2col launch");
 }
 
+int kp_im2col3x3_nhwc_pad(const float* x, int B, int H, int W, int C, float* out, int kpad, void* stream) {
+  if (!x || !out) return fail(KP_EINVAL, "null pointer");
+  if (B < 1 || H < 1 || W < 1 || C < 1) return fail(KP_EINVAL, "bad activation shape");
+  if (kpad < 9 * C || kpad % 4 != 0) return fail(KP_EINVAL, "kpad must be a multiple of 4 and >= 9*C");
+  if ((reinterpret_cast<uintptr_t>(out) & 15) != 0) return fail(KP_EINVAL, "out must be 16-byte aligned");
+  cudaError_t e = kp::im2col3x3_nhwc_pad_launch(x, B, H, W, C, out, kpad, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? KP_OK : cuda_fail(e, "im2col (padded) launch");
+}
+
 int kp_maxpool2x2_nhwc(const float* x, int B, int H, int W, int C, float* out, void* stream) {
   if (!x || !out) return fail(KP_EINVAL, "null pointer");
   if (B < 1 || H < 2 || W < 2 || C < 1) return fail(KP_EINVAL, "bad activation shape");

@@ -49,6 +49,8 @@ void f1_fill_wg9(F1Entry* table);
 cudaError_t im2col3x3_nhwc_launch(const float* x, int B, int H, int W, int C, float* out, int64_t ldo,
                                   cudaStream_t s);
 cudaError_t maxpool2_nhwc_launch(const float* x, int B, int H, int W, int C, float* out, cudaStream_t s);
+cudaError_t im2col3x3_nhwc_pad_launch(const float* x, int B, int H, int W, int C, float* out, int kpad,
+                                      cudaStream_t s);
 
 // FFMA peak probe.
 cudaError_t ffma_peak_launch(float* sink, int blocks, int threads, int iters, bool packed, cudaStream_t s);

@@ -57,6 +57,34 @@ __global__ void im2col3x3_nhwc_vec4_kernel(const float4* __restrict__ x, int B, 
   }
 }
 
+// im2col into rows padded to kpad >= 9C columns (zeros beyond 9C), one thread per float4
+// of a row, 32-bit index math.  For conv1_1 (C = 3, 9C = 27): 28-float rows are 16-byte
+// aligned, so the GEMM takes the vector / TMA operand paths, and the zero column times a
+// zero weight row adds fma(0, 0, acc) == acc -- the chain over the 27 real taps.
+__global__ void im2col3x3_nhwc_pad_kernel(const float* __restrict__ x, int B, int H, int W, int C, int kpad,
+                                          float4* __restrict__ out, unsigned total4) {
+  const unsigned q4 = kpad / 4, K = 9u * C;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total4; i += gridDim.x * blockDim.x) {
+    const unsigned row = i / q4, k0 = (i - row * q4) * 4;
+    const unsigned bh = row / W;
+    const int w = static_cast<int>(row - bh * W);
+    const unsigned b = bh / H;
+    const int h = static_cast<int>(bh - b * H);
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const unsigned kk = k0 + e;
+      v[e] = 0.0f;
+      if (kk < K) {
+        const unsigned tap = kk / C, c = kk - tap * C;
+        const int hy = h + static_cast<int>(tap / 3) - 1, wx = w + static_cast<int>(tap % 3) - 1;
+        if (hy >= 0 && hy < H && wx >= 0 && wx < W) v[e] = __ldg(x + ((static_cast<int64_t>(b) * H + hy) * W + wx) * C + c);
+      }
+    }
+    out[i] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
 // 2x2 / stride 2 max pool, float4 over channels (C % 4 == 0), 32-bit index math.
 __global__ void maxpool2_nhwc_vec4_kernel(const float4* __restrict__ x, int B, int H, int W, int C4,
                                           float4* __restrict__ out, unsigned total) {
@@ -118,6 +146,15 @@ cudaError_t im2col3x3_nhwc_launch(const float* x, int B, int H, int W, int C, fl
     return cudaGetLastError();
   }
   im2col3x3_nhwc_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, B, H, W, C, out, ldo);
+  return cudaGetLastError();
+}
+
+cudaError_t im2col3x3_nhwc_pad_launch(const float* x, int B, int H, int W, int C, float* out, int kpad,
+                                      cudaStream_t s) {
+  const int64_t total4 = static_cast<int64_t>(B) * H * W * (kpad / 4);
+  if (kpad % 4 != 0 || kpad < 9 * C || !aligned16(out) || total4 >= 0x7fffffffLL) return cudaErrorInvalidValue;
+  im2col3x3_nhwc_pad_kernel<<<grid_for(total4, 256), 256, 0, s>>>(x, B, H, W, C, kpad, reinterpret_cast<float4*>(out),
+                                                                   static_cast<unsigned>(total4));
   return cudaGetLastError();
 }
 

@@ -57,6 +57,12 @@ class Vgg16:
         self.device = torch.device(device)
         convs, fcs = weights if weights is not None else init_weights(seed)
         self.convs = [(w.to(self.device).contiguous(), b.to(self.device).contiguous()) for w, b in convs]
+        # conv1_1 (Cin = 3): rows padded from 27 to 28 floats (16-byte aligned, so the GEMM
+        # takes its vector / TMA paths) against a zero 28th weight row: fma(0, 0, acc) ==
+        # acc keeps the fp32 chain over the 27 real taps bit for bit
+        w0, b0 = self.convs[0]
+        self.k_pad0 = (w0.shape[0] + 3) // 4 * 4
+        self.convs[0] = (torch.cat([w0, w0.new_zeros(self.k_pad0 - w0.shape[0], w0.shape[1])]).contiguous(), b0)
         self.fcs = [(w.to(self.device).contiguous(), b.to(self.device).contiguous()) for w, b in fcs]
         B = batch
         # ping-pong activation buffers sized for the largest layer output (B*224*224*64)
@@ -76,7 +82,7 @@ class Vgg16:
                 H //= 2
                 continue
             cin, cout = item
-            out.append(ProblemSize(B * H * H, 9 * cin, cout, 1))
+            out.append(ProblemSize(B * H * H, (9 * cin + 3) // 4 * 4, cout, 1))  # as launched (conv1_1: k 28)
         out += [ProblemSize(B, fin, fout, 1) for fin, fout, _ in VGG16_FC]
         return out
 
@@ -105,8 +111,13 @@ class Vgg16:
                 w, b = self.convs[ci]
                 ci += 1
                 m, k = B * H * H, 9 * cin
-                _lib.check(lib.kp_im2col3x3_nhwc(src.data_ptr(), B, H, H, cin, self.cols.data_ptr(), k,
-                                                 stream_handle), "kp_im2col3x3_nhwc")
+                if k % 4:  # conv1_1: 16-byte-aligned padded rows
+                    k = self.k_pad0
+                    _lib.check(lib.kp_im2col3x3_nhwc_pad(src.data_ptr(), B, H, H, cin, self.cols.data_ptr(), k,
+                                                         stream_handle), "kp_im2col3x3_nhwc_pad")
+                else:
+                    _lib.check(lib.kp_im2col3x3_nhwc(src.data_ptr(), B, H, H, cin, self.cols.data_ptr(), k,
+                                                     stream_handle), "kp_im2col3x3_nhwc")
                 self._gemm(self.cols, w, b, dst, m, k, cout, True, stream_handle)
                 C = cout
             src = dst
@@ -143,4 +154,7 @@ class Vgg16:
 
     @property
     def flops(self) -> int:
-        return sum(p.flops for p in self.problems()) + 0  # GEMM flops (duplicates counted per layer)
+        """Convolution + fc flops of one forward (conv1_1 counted at its true k = 27)."""
+        probs = self.problems()
+        first = probs[0]
+        return sum(p.flops for p in probs) - 2 * first.m * first.n * (first.k - 27)

@@ -45,6 +45,20 @@ def test_im2col_and_pool_exact(cuda_device):
     assert np.array_equal(pout.cpu().numpy(), vgg16_ref.maxpool2(y))
 
 
+@pytest.mark.parametrize("B,H,W,C,kpad", [(2, 9, 7, 3, 28), (1, 6, 5, 3, 32), (2, 4, 4, 8, 72)])
+def test_im2col_padded_rows(cuda_device, B, H, W, C, kpad):
+    """kp_im2col3x3_nhwc_pad: the 9C patch values then zeros up to kpad in every row."""
+    lib = _lib.load()
+    x = np.random.default_rng(kpad).standard_normal((B, H, W, C)).astype(np.float32)
+    out = torch.full((B * H * W, kpad), 7.0, device=cuda_device)
+    assert lib.kp_im2col3x3_nhwc_pad(torch.from_numpy(x).to(cuda_device).data_ptr(), B, H, W, C, out.data_ptr(),
+                                     kpad, None) == 0
+    got = out.cpu().numpy()
+    assert np.array_equal(got[:, :9 * C], vgg16_ref.im2col3x3(x))
+    assert not got[:, 9 * C:].any()
+    assert lib.kp_im2col3x3_nhwc_pad(0, B, H, W, C, out.data_ptr(), 27, None) == _lib.KP_EINVAL
+
+
 @pytest.mark.parametrize("B,H,W,C", [(2, 9, 7, 8), (3, 14, 14, 64), (1, 5, 6, 512)])
 def test_im2col_and_pool_vec4_exact(cuda_device, B, H, W, C):
     """The float4 kernels (C % 4 == 0, every VGG16 layer after conv1_1), ldo > 9C too."""

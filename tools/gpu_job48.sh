@@ -1,0 +1,7 @@
+mkdir -p gpurun_out/job48
+make -s -C oracle
+timeout 900 python -m pytest tests/test_vgg16_gpu.py -q -x > gpurun_out/job48/pytest.log 2>&1; tail -3 gpurun_out/job48/pytest.log
+for B in 1 16 64; do
+  timeout 900 python bench.py --workload vgg16-infer --batch $B --steps 20 > gpurun_out/job48/vgg16_b$B.json 2>&1
+  timeout 900 python bench.py --workload vgg16-infer --family tf32 --table data/sweeps/vgg16_tf32.csv --batch $B --steps 20 > gpurun_out/job48/vgg16_tf32_b$B.json 2>&1
+done
