@@ -140,6 +140,17 @@ int kp_bench(int id, int m, int k, int n, int batch,
              int warmup, int min_iters, int max_iters, double min_ms,
              double* mean_ms, int* iters, void* stream);
 
+/* The sweep protocol: like kp_bench, but launch i uses operand set i mod
+ * n_sets (A[i], B[i], C[i]; same shape and strides) -- rotating through more data than
+ * L2 holds keeps small problems from being timed with a warm cache -- and the timed loop
+ * runs `repeats` times; *median_ms is the median of the per-launch means. */
+int kp_bench_sets(int id, int m, int k, int n, int batch, int n_sets,
+                  const void* const* A, int64_t lda, int64_t sA,
+                  const void* const* B, int64_t ldb, int64_t sB,
+                  void* const* C, int64_t ldc, int64_t sC,
+                  int warmup, int min_iters, int max_iters, double min_ms, int repeats,
+                  double* median_ms, int* iters, void* stream);
+
 /* Peak FP32 throughput probe: register-resident FMA chains on every SM, scalar
  * FFMA (packed = 0) or sm_100 packed FFMA2 (packed = 1); returns TFLOP/s in *tflops
  * (the measured FP32 SIMT peak the SIMT families' roofline fraction uses). */

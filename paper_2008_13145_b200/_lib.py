@@ -54,6 +54,7 @@ _vp = ctypes.c_void_p
 _dp = ctypes.POINTER(ctypes.c_double)
 _ip = ctypes.POINTER(ctypes.c_int)
 _i32p = ctypes.POINTER(ctypes.c_int32)
+_vpp = ctypes.POINTER(ctypes.c_void_p)
 
 _GEMM_ARGS = [_i, _i, _i, _i, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64]
 
@@ -71,6 +72,8 @@ SIGNATURES = {
     "kp_set_max_k_slices": (_i, [_i]),
     "kp_gemm_plan": (_i, [_i, _i, _i, _i, _i, _i, _ip, _ip]),
     "kp_bench": (_i, [_i] + _GEMM_ARGS + [_i, _i, _i, ctypes.c_double, _dp, _ip, _vp]),
+    "kp_bench_sets": (_i, [_i, _i, _i, _i, _i, _i, _vpp, _i64, _i64, _vpp, _i64, _i64, _vpp, _i64, _i64,
+                           _i, _i, _i, ctypes.c_double, _i, _dp, _ip, _vp]),
     "kp_ffma_peak": (_i, [_i, _dp, _vp]),
     "kp_dispatch_load": (_i, [_i, _i32p, _dp, _i32p, _i32p, _i32p, _i, _i32p]),
     "kp_dispatch_free": (_i, [_i]),

@@ -1,5 +1,6 @@
 // The C ABI of libkpgemm.so (include/kpgemm.h): variant registry, GEMM launch,
 // benchmark harness, FFMA peak probe and the tree -> variant dispatch tables.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -408,17 +409,24 @@ int kp_gemm_plan(int id, int m, int k, int n, int batch, int num_sms, int* k_sli
   return KP_OK;
 }
 
-int kp_bench(int id, int m, int k, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* B,
-             int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, int warmup, int min_iters, int max_iters,
-             double min_ms, double* mean_ms, int* iters, void* stream) {
-  int rc = check_problem(id, m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC);
-  if (rc != KP_OK) return rc;
-  if (!mean_ms || !iters) return fail(KP_EINVAL, "null output pointer");
+int kp_bench_sets(int id, int m, int k, int n, int batch, int n_sets, const void* const* A, int64_t lda, int64_t sA,
+                  const void* const* B, int64_t ldb, int64_t sB, void* const* C, int64_t ldc, int64_t sC, int warmup,
+                  int min_iters, int max_iters, double min_ms, int repeats, double* median_ms, int* iters,
+                  void* stream) {
+  if (n_sets < 1 || !A || !B || !C) return fail(KP_EINVAL, "need at least one operand set");
+  if (repeats < 1 || repeats > 64) return fail(KP_EINVAL, "repeats must be in [1, 64]");
+  if (!median_ms || !iters) return fail(KP_EINVAL, "null output pointer");
   if (min_iters < 1 || max_iters < min_iters) return fail(KP_EINVAL, "bad iteration bounds");
+  std::vector<kp::GemmArgs> sets;
+  for (int i = 0; i < n_sets; ++i) {
+    int rc = check_problem(id, m, k, n, batch, A[i], lda, sA, B[i], ldb, sB, C[i], ldc, sC);
+    if (rc != KP_OK) return rc;
+    sets.push_back(make_args(m, k, n, batch, A[i], lda, sA, B[i], ldb, sB, C[i], ldc, sC));
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const kp::GemmArgs p = make_args(m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC);
+  int rc = KP_OK;
   for (int i = 0; i < warmup; ++i)
-    if ((rc = launch(id, p, s)) != KP_OK) return rc;
+    if ((rc = launch(id, sets[i % n_sets], s)) != KP_OK) return rc;
   cudaEvent_t e0, e1;
   cudaError_t e;
   if ((e = cudaEventCreate(&e0)) != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
@@ -426,10 +434,12 @@ int kp_bench(int id, int m, int k, int n, int batch, const void* A, int64_t lda,
     cudaEventDestroy(e0);
     return cuda_fail(e, "cudaEventCreate");
   }
+  int next = 0;  // launches rotate through the operand sets
   auto timed = [&](int count, float* ms) -> int {
     cudaEventRecord(e0, s);
     for (int i = 0; i < count; ++i) {
-      int r = launch(id, p, s);
+      int r = launch(id, sets[next], s);
+      next = (next + 1) % n_sets;
       if (r != KP_OK) return r;
     }
     cudaEventRecord(e1, s);
@@ -439,25 +449,38 @@ int kp_bench(int id, int m, int k, int n, int batch, const void* A, int64_t lda,
     if (err != cudaSuccess) return cuda_fail(err, "cudaEventElapsedTime");
     return KP_OK;
   };
-  float t1 = 0.f, tn = 0.f;
+  float t1 = 0.f;
   rc = timed(1, &t1);
   int count = min_iters;
+  std::vector<double> means;
   if (rc == KP_OK) {
-    if (min_iters <= 1 && t1 >= min_ms) {
-      tn = t1;  // a launch that alone fills the time budget is its own measurement
+    if (repeats == 1 && min_iters <= 1 && t1 >= min_ms) {
+      means.push_back(t1);  // a launch that alone fills the time budget is its own measurement
       count = 1;
     } else {
       const double want = t1 > 0.f ? std::ceil(min_ms / t1) : static_cast<double>(max_iters);
       count = static_cast<int>(want < min_iters ? min_iters : (want > max_iters ? max_iters : want));
-      rc = timed(count, &tn);
+      for (int r = 0; r < repeats && rc == KP_OK; ++r) {
+        float tn = 0.f;
+        rc = timed(count, &tn);
+        means.push_back(static_cast<double>(tn) / count);
+      }
     }
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (rc != KP_OK) return rc;
-  *mean_ms = static_cast<double>(tn) / count;
+  std::sort(means.begin(), means.end());
+  *median_ms = means[means.size() / 2];
   *iters = count;
   return KP_OK;
+}
+
+int kp_bench(int id, int m, int k, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* B,
+             int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, int warmup, int min_iters, int max_iters,
+             double min_ms, double* mean_ms, int* iters, void* stream) {
+  return kp_bench_sets(id, m, k, n, batch, 1, &A, lda, sA, &B, ldb, sB, &C, ldc, sC, warmup, min_iters, max_iters,
+                       min_ms, 1, mean_ms, iters, stream);
 }
 
 int kp_ffma_peak(int packed, double* tflops, void* stream) {

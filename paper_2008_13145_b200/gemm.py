@@ -175,6 +175,26 @@ def bench(vid: int, ops: GemmOperands, warmup: int = 1, min_iters: int = 2, max_
     return mean.value, iters.value
 
 
+def bench_sets(vid: int, sets: list[GemmOperands], warmup: int = 2, min_iters: int = 1, max_iters: int = 10000,
+               min_ms: float = 1.0, repeats: int = 3, stream: torch.cuda.Stream | None = None) -> tuple[float, int]:
+    """Median over ``repeats`` timed loops of the per-launch mean (ms), launches rotating
+    through operand ``sets`` of one shape (``kp_bench_sets``; SURVEY 8(d) protocol)."""
+    lib = _lib.load()
+    first = sets[0]
+    s = (stream or torch.cuda.current_stream(first.A.device)).cuda_stream
+    n = len(sets)
+    A = (ctypes.c_void_p * n)(*[o.A.data_ptr() for o in sets])
+    B = (ctypes.c_void_p * n)(*[o.B.data_ptr() for o in sets])
+    C = (ctypes.c_void_p * n)(*[o.C.data_ptr() for o in sets])
+    med = ctypes.c_double()
+    iters = ctypes.c_int()
+    _lib.check(lib.kp_bench_sets(vid, first.m, first.k, first.n, first.batch, n, A, first.lda, first.sA, B, first.ldb,
+                                 first.sB, C, first.ldc, first.sC, warmup, min_iters, max_iters, float(min_ms),
+                                 repeats, ctypes.byref(med), ctypes.byref(iters), s),
+               f"kp_bench_sets(variant {vid}, {first.problem})")
+    return med.value, iters.value
+
+
 def k_slice_plan(config: KernelConfig | int, problem: ProblemSize, family: str = "simt",
                  num_sms: int = 0) -> tuple[int, int]:
     """(k_slices, k_per_slice) the library uses for this launch (kp_gemm_plan):

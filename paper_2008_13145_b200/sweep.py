@@ -73,13 +73,16 @@ class SynthTimer:
 class CudaEventTimer:
     """Times kernel-library variants with CUDA events through ``kp_bench``.
 
-    One set of operand buffers sized for the largest problem is allocated up front
-    and reused for every cell (inputs U(-1, 1), seed 0).  ``min_ms`` bounds the timed
-    loop; a launch that alone exceeds it is timed once.
+    Protocol (adapted from PAPER.md:238-246): warm-up launches, then
+    ``repeats`` CUDA-event loops of >= ``min_ms / repeats`` each; the cell's time is the
+    median of the loops' per-launch means.  A problem whose operands total less than
+    twice the L2 is timed rotating through enough copies of its operands to cover
+    2 x L2, so small problems are not measured with a warm cache.  One set of buffers
+    sized for the largest problem (U(-1, 1), seed 0) holds every copy.
     """
 
-    def __init__(self, family: str, problems, warmup: int = 1, min_ms: float = 5.0,
-                 max_iters: int = 2000, device: int = 0, seed: int = 0):
+    def __init__(self, family: str, problems, warmup: int = 2, min_ms: float = 5.0,
+                 max_iters: int = 2000, device: int = 0, seed: int = 0, repeats: int = 3):
         import torch  # imported lazily: CPU-only callers never need it
 
         from . import gemm
@@ -88,12 +91,15 @@ class CudaEventTimer:
         self.gemm = gemm
         self.family = family
         self.configs = gemm.family_configs(family)
-        self.warmup, self.min_ms, self.max_iters = warmup, min_ms, max_iters
+        self.warmup, self.min_ms, self.max_iters, self.repeats = warmup, min_ms, max_iters, repeats
+        self.l2_bytes = torch.cuda.get_device_properties(torch.device("cuda", device)).L2_cache_size
         self.device = torch.device("cuda", device)
         dtype = gemm.input_dtype(family)
-        max_a = max(p.batch * p.m * p.k for p in problems)
-        max_b = max(p.batch * p.k * p.n for p in problems)
-        max_c = max(p.batch * p.m * p.n for p in problems)
+        # every buffer holds at least 2 x L2 of copies (operand rotation), plus alignment slack
+        floor = (2 * self.l2_bytes) // gemm.input_dtype(family).itemsize + 64 * 64
+        max_a = max(floor, max(p.batch * p.m * p.k for p in problems))
+        max_b = max(floor, max(p.batch * p.k * p.n for p in problems))
+        max_c = max(floor, max(p.batch * p.m * p.n for p in problems))
         gen = torch.Generator(device=self.device).manual_seed(seed)
         self.bufA = (torch.rand(max_a, device=self.device, generator=gen) * 2 - 1).to(dtype)
         self.bufB = (torch.rand(max_b, device=self.device, generator=gen) * 2 - 1).to(dtype)
@@ -126,19 +132,30 @@ class CudaEventTimer:
             return "", ""
 
     def operands(self, problem: ProblemSize):
+        """Operand sets for the problem: one, or enough copies to cover 2 x L2."""
         if self._ops_key != problem:
             p = problem
-            A = self.bufA[: p.batch * p.m * p.k].view(p.batch, p.m, p.k)
-            B = self.bufB[: p.batch * p.k * p.n].view(p.batch, p.k, p.n)
-            C = self.bufC[: p.batch * p.m * p.n].view(p.batch, p.m, p.n)
-            self._ops = self.gemm.GemmOperands(A, B, C, A.dtype)
+            na, nb, nc = p.batch * p.m * p.k, p.batch * p.k * p.n, p.batch * p.m * p.n
+            foot = na * self.bufA.element_size() + nb * self.bufB.element_size() + nc * 4
+            sets = 1 if foot >= 2 * self.l2_bytes else math.ceil(2 * self.l2_bytes / foot)
+            pad = lambda x: (x + 63) // 64 * 64  # noqa: E731  (256-byte aligned copies)
+            sets = max(1, min(sets, 64, self.bufA.numel() // pad(na), self.bufB.numel() // pad(nb),
+                              self.bufC.numel() // pad(nc)))
+            ops = []
+            for i in range(sets):
+                A = self.bufA[i * pad(na): i * pad(na) + na].view(p.batch, p.m, p.k)
+                B = self.bufB[i * pad(nb): i * pad(nb) + nb].view(p.batch, p.k, p.n)
+                C = self.bufC[i * pad(nc): i * pad(nc) + nc].view(p.batch, p.m, p.n)
+                ops.append(self.gemm.GemmOperands(A, B, C, A.dtype))
+            self._ops = ops
             self._ops_key = problem
         return self._ops
 
     def __call__(self, problem: ProblemSize, config_index: int) -> tuple[float, float, int]:
         vid = self.gemm.variant_id(self.configs[config_index], self.family)
-        ms, iters = self.gemm.bench(vid, self.operands(problem), warmup=self.warmup, min_iters=1,
-                                    max_iters=self.max_iters, min_ms=self.min_ms, stream=self.stream)
+        ms, iters = self.gemm.bench_sets(vid, self.operands(problem), warmup=self.warmup, min_iters=1,
+                                         max_iters=self.max_iters, min_ms=self.min_ms / self.repeats,
+                                         repeats=self.repeats, stream=self.stream)
         if not (ms > 0.0 and math.isfinite(ms)):
             raise DataError(f"non-positive time for {problem} / config {config_index}")
         return problem.flops / (ms * 1e-3) / 1e9, ms, iters
