@@ -228,3 +228,22 @@ def test_bad_operands_raise(cuda_device):
         gemm.matmul(A.cpu(), torch.rand(4, 3), cfg)
     with pytest.raises(KeyError):
         gemm.matmul(A, torch.rand(4, 3, device=cuda_device), KernelConfig(3, 1, 1, 8, 8))
+
+
+def test_bench_sets_rotation_and_median(cuda_device):
+    """kp_bench_sets (the sweep's protocol): rotating operand sets, median of repeats;
+    every set's C receives the product; bad arguments are rejected."""
+    m, k, n = 96, 64, 80
+    sets = []
+    for i in range(3):
+        A = torch.rand(m, k, device=cuda_device)
+        B = torch.rand(k, n, device=cuda_device)
+        C = torch.zeros(m, n, device=cuda_device)
+        sets.append(gemm.GemmOperands(A, B, C, torch.float32))
+    vid = gemm.variant_id(KernelConfig(4, 4, 4, 16, 16), "simt")
+    ms, iters = gemm.bench_sets(vid, sets, warmup=2, min_ms=0.2, repeats=3)
+    assert ms > 0 and iters >= 1
+    for o in sets:
+        assert torch.allclose(o.C[0], o.A[0] @ o.B[0], rtol=1e-5, atol=1e-5)
+    with pytest.raises(ValueError):
+        gemm.bench_sets(vid, sets, repeats=0)
