@@ -195,6 +195,11 @@ int kp_im2col3x3_nhwc(const float* x, int B, int H, int W, int C, float* out, in
  * families read with their vector / TMA paths (pair it with a zero-padded weight row:
  * fma(0, 0, acc) == acc, so the fp32 chain is unchanged). */
 int kp_im2col3x3_nhwc_pad(const float* x, int B, int H, int W, int C, float* out, int kpad, void* stream);
+/* bf16 operands for the BF16 family: the same patches as bf16 rows of kpad columns
+ * (kpad % 8 == 0, >= 9*C; zeros beyond 9*C; round to nearest even), and an fp32 -> bf16
+ * cast of n elements (n % 8 == 0, 16-byte-aligned pointers). */
+int kp_im2col3x3_nhwc_bf16(const float* x, int B, int H, int W, int C, void* out, int kpad, void* stream);
+int kp_cast_bf16(const float* x, int64_t n, void* out, void* stream);
 /* 2x2 / stride 2 max pooling, NHWC: (B, H, W, C) -> (B, H/2, W/2, C). */
 int kp_maxpool2x2_nhwc(const float* x, int B, int H, int W, int C, float* out, void* stream);
 

@@ -530,6 +530,20 @@ int kp_im2col3x3_nhwc_pad(const float* x, int B, int H, int W, int C, float* out
   return e == cudaSuccess ? KP_OK : cuda_fail(e, "im2col (padded) launch");
 }
 
+int kp_im2col3x3_nhwc_bf16(const float* x, int B, int H, int W, int C, void* out, int kpad, void* stream) {
+  if (!x || !out) return fail(KP_EINVAL, "null pointer");
+  if (B < 1 || H < 1 || W < 1 || C < 1) return fail(KP_EINVAL, "bad activation shape");
+  if (kpad < 9 * C || kpad % 8 != 0) return fail(KP_EINVAL, "kpad must be a multiple of 8 and >= 9*C");
+  cudaError_t e = kp::im2col3x3_nhwc_bf16_launch(x, B, H, W, C, out, kpad, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? KP_OK : cuda_fail(e, "im2col (bf16) launch");
+}
+
+int kp_cast_bf16(const float* x, int64_t n, void* out, void* stream) {
+  if (!x || !out || n < 1) return fail(KP_EINVAL, "bad cast arguments");
+  cudaError_t e = kp::cast_bf16_launch(x, n, out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? KP_OK : cuda_fail(e, "bf16 cast launch (n % 8 == 0, 16-byte aligned)");
+}
+
 int kp_maxpool2x2_nhwc(const float* x, int B, int H, int W, int C, float* out, void* stream) {
   if (!x || !out) return fail(KP_EINVAL, "null pointer");
   if (B < 1 || H < 2 || W < 2 || C < 1) return fail(KP_EINVAL, "bad activation shape");

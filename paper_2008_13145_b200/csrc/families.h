@@ -51,6 +51,9 @@ cudaError_t im2col3x3_nhwc_launch(const float* x, int B, int H, int W, int C, fl
 cudaError_t maxpool2_nhwc_launch(const float* x, int B, int H, int W, int C, float* out, cudaStream_t s);
 cudaError_t im2col3x3_nhwc_pad_launch(const float* x, int B, int H, int W, int C, float* out, int kpad,
                                       cudaStream_t s);
+cudaError_t im2col3x3_nhwc_bf16_launch(const float* x, int B, int H, int W, int C, void* out, int kpad,
+                                       cudaStream_t s);
+cudaError_t cast_bf16_launch(const float* x, int64_t n, void* out, cudaStream_t s);
 
 // FFMA peak probe.
 cudaError_t ffma_peak_launch(float* sink, int blocks, int threads, int iters, bool packed, cudaStream_t s);

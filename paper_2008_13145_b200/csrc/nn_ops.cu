@@ -7,8 +7,15 @@
 // pass.  NHWC keeps the GEMM output (B*H*W) x Cout equal to the next layer's input.
 #include "families.h"
 
+#include <cuda_bf16.h>
+
 namespace kp {
 namespace {
+
+__device__ __forceinline__ unsigned pack_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo (low half), .y = hi
+  return *reinterpret_cast<const unsigned*>(&v);
+}
 
 // One thread per output element; consecutive threads walk k = (dy*3 + dx)*C + c, so
 // both the gather (contiguous channels of one tap) and the store are coalesced.
@@ -85,6 +92,61 @@ __global__ void im2col3x3_nhwc_pad_kernel(const float* __restrict__ x, int B, in
   }
 }
 
+// bf16 operands for the BF16 tensor-core family: im2col of fp32 NHWC activations into
+// kpad-wide bf16 rows (zeros beyond 9C), one thread per 8 columns (one 16-byte store);
+// the 8 columns are one tap's contiguous channels when C % 8 == 0 (two float4 loads),
+// else gathered one by one (conv1_1, C = 3).
+__global__ void im2col3x3_nhwc_bf16_kernel(const float* __restrict__ x, int B, int H, int W, int C, int kpad,
+                                           uint4* __restrict__ out, unsigned total8) {
+  const unsigned q8 = kpad / 8, K = 9u * C;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total8; i += gridDim.x * blockDim.x) {
+    const unsigned row = i / q8, k0 = (i - row * q8) * 8;
+    const unsigned bh = row / W;
+    const int w = static_cast<int>(row - bh * W);
+    const unsigned b = bh / H;
+    const int h = static_cast<int>(bh - b * H);
+    float v[8];
+    if (C % 8 == 0 && k0 + 8 <= K) {
+      const unsigned tap = k0 / C, c = k0 - tap * C;
+      const int hy = h + static_cast<int>(tap / 3) - 1, wx = w + static_cast<int>(tap % 3) - 1;
+      if (hy >= 0 && hy < H && wx >= 0 && wx < W) {
+        const float4* src = reinterpret_cast<const float4*>(x + ((static_cast<int64_t>(b) * H + hy) * W + wx) * C + c);
+        const float4 a = __ldg(src), d = __ldg(src + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = d.x; v[5] = d.y; v[6] = d.z; v[7] = d.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = 0.0f;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const unsigned kk = k0 + e;
+        v[e] = 0.0f;
+        if (kk < K) {
+          const unsigned tap = kk / C, c = kk - tap * C;
+          const int hy = h + static_cast<int>(tap / 3) - 1, wx = w + static_cast<int>(tap % 3) - 1;
+          if (hy >= 0 && hy < H && wx >= 0 && wx < W)
+            v[e] = __ldg(x + ((static_cast<int64_t>(b) * H + hy) * W + wx) * C + c);
+        }
+      }
+    }
+    uint4 o;
+    o.x = pack_bf16x2(v[0], v[1]);
+    o.y = pack_bf16x2(v[2], v[3]);
+    o.z = pack_bf16x2(v[4], v[5]);
+    o.w = pack_bf16x2(v[6], v[7]);
+    out[i] = o;
+  }
+}
+
+// fp32 -> bf16 (round to nearest even), 8 elements per thread (n % 8 == 0, 16-byte aligned).
+__global__ void cast_bf16_kernel(const float4* __restrict__ x, uint4* __restrict__ out, unsigned total8) {
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total8; i += gridDim.x * blockDim.x) {
+    const float4 a = __ldg(x + 2 * i), d = __ldg(x + 2 * i + 1);
+    out[i] = make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(d.x, d.y), pack_bf16x2(d.z, d.w));
+  }
+}
+
 // 2x2 / stride 2 max pool, float4 over channels (C % 4 == 0), 32-bit index math.
 __global__ void maxpool2_nhwc_vec4_kernel(const float4* __restrict__ x, int B, int H, int W, int C4,
                                           float4* __restrict__ out, unsigned total) {
@@ -155,6 +217,24 @@ cudaError_t im2col3x3_nhwc_pad_launch(const float* x, int B, int H, int W, int C
   if (kpad % 4 != 0 || kpad < 9 * C || !aligned16(out) || total4 >= 0x7fffffffLL) return cudaErrorInvalidValue;
   im2col3x3_nhwc_pad_kernel<<<grid_for(total4, 256), 256, 0, s>>>(x, B, H, W, C, kpad, reinterpret_cast<float4*>(out),
                                                                    static_cast<unsigned>(total4));
+  return cudaGetLastError();
+}
+
+cudaError_t im2col3x3_nhwc_bf16_launch(const float* x, int B, int H, int W, int C, void* out, int kpad,
+                                       cudaStream_t s) {
+  const int64_t total8 = static_cast<int64_t>(B) * H * W * (kpad / 8);
+  if (kpad % 8 != 0 || kpad < 9 * C || !aligned16(out) || total8 >= 0x7fffffffLL ||
+      (C % 8 == 0 && !aligned16(x)))
+    return cudaErrorInvalidValue;
+  im2col3x3_nhwc_bf16_kernel<<<grid_for(total8, 256), 256, 0, s>>>(x, B, H, W, C, kpad, reinterpret_cast<uint4*>(out),
+                                                                    static_cast<unsigned>(total8));
+  return cudaGetLastError();
+}
+
+cudaError_t cast_bf16_launch(const float* x, int64_t n, void* out, cudaStream_t s) {
+  if (n % 8 != 0 || !aligned16(x) || !aligned16(out) || n / 8 >= 0x7fffffffLL) return cudaErrorInvalidValue;
+  cast_bf16_kernel<<<grid_for(n / 8, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<uint4*>(out),
+                                                         static_cast<unsigned>(n / 8));
   return cudaGetLastError();
 }
 

@@ -56,19 +56,27 @@ class Vgg16:
         self.batch = batch
         self.device = torch.device(device)
         convs, fcs = weights if weights is not None else init_weights(seed)
+        # BF16 family: bf16 weights and im2col rows (fp32 accumulation, fp32 activations in
+        # between -- the GEMM epilogue writes fp32 and the next im2col rounds to bf16)
+        self.bf16 = dispatcher.family == "bf16"
+        wdt = torch.bfloat16 if self.bf16 else torch.float32
         self.convs = [(w.to(self.device).contiguous(), b.to(self.device).contiguous()) for w, b in convs]
         # conv1_1 (Cin = 3): rows padded from 27 to 28 floats (16-byte aligned, so the GEMM
         # takes its vector / TMA paths) against a zero 28th weight row: fma(0, 0, acc) ==
-        # acc keeps the fp32 chain over the 27 real taps bit for bit
+        # acc keeps the fp32 chain over the 27 real taps bit for bit (32 for bf16 rows)
         w0, b0 = self.convs[0]
-        self.k_pad0 = (w0.shape[0] + 3) // 4 * 4
+        align = 8 if self.bf16 else 4
+        self.k_pad0 = (w0.shape[0] + align - 1) // align * align
         self.convs[0] = (torch.cat([w0, w0.new_zeros(self.k_pad0 - w0.shape[0], w0.shape[1])]).contiguous(), b0)
-        self.fcs = [(w.to(self.device).contiguous(), b.to(self.device).contiguous()) for w, b in fcs]
+        self.convs = [(w.to(wdt).contiguous(), b) for w, b in self.convs]
+        self.fcs = [(w.to(self.device).to(wdt).contiguous(), b.to(self.device).contiguous()) for w, b in fcs]
         B = batch
         # ping-pong activation buffers sized for the largest layer output (B*224*224*64)
         act = B * 224 * 224 * 64
         self.act = [torch.empty(act, device=self.device) for _ in range(2)]
-        self.cols = torch.empty(B * 224 * 224 * 9 * 64, device=self.device)  # conv1_2 im2col
+        self.cols = torch.empty(B * 224 * 224 * 9 * 64, device=self.device, dtype=wdt)  # conv1_2 im2col
+        self.fc_in = torch.empty(B, 7 * 7 * 512, device=self.device, dtype=wdt)  # bf16 fc operands
+        self.fc_in2 = torch.empty(B, 4096, device=self.device, dtype=wdt)
         self.input = torch.empty(B, 224, 224, 3, device=self.device)
         self.logits = torch.empty(B, 1000, device=self.device)
         self.fc_buf = [torch.empty(B, 4096, device=self.device) for _ in range(2)]
@@ -82,7 +90,8 @@ class Vgg16:
                 H //= 2
                 continue
             cin, cout = item
-            out.append(ProblemSize(B * H * H, (9 * cin + 3) // 4 * 4, cout, 1))  # as launched (conv1_1: k 28)
+            align = 8 if getattr(self, "bf16", False) else 4
+            out.append(ProblemSize(B * H * H, (9 * cin + align - 1) // align * align, cout, 1))  # as launched
         out += [ProblemSize(B, fin, fout, 1) for fin, fout, _ in VGG16_FC]
         return out
 
@@ -111,7 +120,11 @@ class Vgg16:
                 w, b = self.convs[ci]
                 ci += 1
                 m, k = B * H * H, 9 * cin
-                if k % 4:  # conv1_1: 16-byte-aligned padded rows
+                if self.bf16:
+                    k = k if k % 8 == 0 else self.k_pad0
+                    _lib.check(lib.kp_im2col3x3_nhwc_bf16(src.data_ptr(), B, H, H, cin, self.cols.data_ptr(), k,
+                                                          stream_handle), "kp_im2col3x3_nhwc_bf16")
+                elif k % 4:  # conv1_1: 16-byte-aligned padded rows
                     k = self.k_pad0
                     _lib.check(lib.kp_im2col3x3_nhwc_pad(src.data_ptr(), B, H, H, cin, self.cols.data_ptr(), k,
                                                          stream_handle), "kp_im2col3x3_nhwc_pad")
@@ -125,6 +138,10 @@ class Vgg16:
         x = src  # (B, 7, 7, 512) NHWC flattened per image = fc6 input rows
         for j, ((fin, fout, relu), (w, b)) in enumerate(zip(VGG16_FC, self.fcs)):
             out = self.logits if j == len(self.fcs) - 1 else self.fc_buf[j % 2]
+            if self.bf16:
+                xin = self.fc_in if j == 0 else self.fc_in2
+                _lib.check(lib.kp_cast_bf16(x.data_ptr(), B * fin, xin.data_ptr(), stream_handle), "kp_cast_bf16")
+                x = xin
             self._gemm(x, w, b, out, B, fin, fout, relu, stream_handle)
             x = out
         return self.logits

@@ -118,3 +118,46 @@ def test_vgg16_forward_tf32_family_within_tolerance(cuda_device):
     rel = np.linalg.norm(got - want) / np.linalg.norm(want)
     assert rel < 2e-2, rel
     assert not np.array_equal(got, want)  # it really ran on the tensor cores
+
+
+def test_vgg16_forward_bf16_family_within_tolerance(cuda_device):
+    """VGG16 inference on the tcgen05 BF16 family: bf16 weights and im2col rows
+    (kp_im2col3x3_nhwc_bf16, kp_cast_bf16 for the fc inputs), fp32 accumulation and fp32
+    activations between layers; logits within 5e-2 normwise of the fp32 oracle forward
+    (bf16 keeps 8 significant bits: ~2^-9 relative rounding per operand per layer)."""
+    from paper_2008_13145_b200 import gemm
+    from paper_2008_13145_b200.classify import TreeModel
+    from paper_2008_13145_b200.selection import ConfigSubset
+
+    cfgs = gemm.family_configs("bf16")
+    leaf = TreeModel(feature=np.array([-1]), threshold=np.array([np.nan]), left=np.array([-1]),
+                     right=np.array([-1]), leaf_class=np.array([0]))
+    disp = Dispatcher(leaf, ConfigSubset((2,), "fixed", 1, 1), cfgs, "bf16")  # (128,64,256,4,192)
+    convs, fcs = vgg16.init_weights(seed=0)
+    model = vgg16.Vgg16(disp, 1, cuda_device, weights=(convs, fcs))
+    x = torch.randn(1, 224, 224, 3, generator=torch.Generator().manual_seed(7))
+    got = model.forward(x.to(cuda_device)).double().cpu().numpy()
+    want = vgg16_ref.forward(x.numpy(), [(w.numpy(), b.numpy()) for w, b in convs],
+                             [(w.numpy(), b.numpy()) for w, b in fcs]).astype(np.float64)
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+    print(f"bf16 VGG16 normwise relative error {rel:.3e}")
+    assert rel < 5e-2, rel
+
+
+def test_bf16_operand_kernels(cuda_device):
+    lib = _lib.load()
+    x = torch.randn(2, 5, 6, 8, device=cuda_device)
+    k = 72
+    out = torch.empty(2 * 5 * 6, k, device=cuda_device, dtype=torch.bfloat16)
+    assert lib.kp_im2col3x3_nhwc_bf16(x.data_ptr(), 2, 5, 6, 8, out.data_ptr(), k, None) == 0
+    want = torch.from_numpy(vgg16_ref.im2col3x3(x.cpu().numpy())).to(torch.bfloat16)
+    assert torch.equal(out.cpu(), want)
+    x3 = torch.randn(1, 4, 4, 3, device=cuda_device)
+    out3 = torch.full((16, 32), 9.0, device=cuda_device, dtype=torch.bfloat16)
+    assert lib.kp_im2col3x3_nhwc_bf16(x3.data_ptr(), 1, 4, 4, 3, out3.data_ptr(), 32, None) == 0
+    want3 = torch.from_numpy(vgg16_ref.im2col3x3(x3.cpu().numpy())).to(torch.bfloat16)
+    assert torch.equal(out3[:, :27].cpu(), want3) and not out3[:, 27:].float().any()
+    v = torch.randn(64, device=cuda_device)
+    c = torch.empty(64, device=cuda_device, dtype=torch.bfloat16)
+    assert lib.kp_cast_bf16(v.data_ptr(), 64, c.data_ptr(), None) == 0
+    assert torch.equal(c, v.to(torch.bfloat16))
