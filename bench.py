@@ -299,11 +299,12 @@ def run_ours(args, world, rank, local):
     disp = Dispatcher(tree, subset, pm.configs, args.family)
 
     layers = vgg16_layers(args.batch)
+    in_dtype = gemm.input_dtype(args.family)  # fp32, or bf16 operands for the BF16 family
     gen = torch.Generator(device=device).manual_seed(1234 + rank)
     bufs = []
     for name, p in layers:
-        A = torch.rand(p.m, p.k, device=device, generator=gen) * 2 - 1
-        W = (torch.rand(p.k, p.n, device=device, generator=gen) * 2 - 1) * math.sqrt(6.0 / p.k)
+        A = (torch.rand(p.m, p.k, device=device, generator=gen) * 2 - 1).to(in_dtype)
+        W = ((torch.rand(p.k, p.n, device=device, generator=gen) * 2 - 1) * math.sqrt(6.0 / p.k)).to(in_dtype)
         C = torch.empty(p.m, p.n, device=device)
         bufs.append((name, p, A, W, C, disp.variant(p)))
     step_flops = sum(p.flops for _, p in layers)
@@ -355,7 +356,16 @@ def run_ours(args, world, rank, local):
     dom_ms = dg["ms"] / dg["launches"]
     dom_cfg, dom_fam = gemm.variant_info(dvid)
     dname = "+".join(dg["names"])
-    peak = gemm.ffma_peak_tflops(packed=True)
+    tensor = dom_fam in ("tf32", "bf16")
+    if tensor:  # tensor-pipe roofline: MEASURED_PEAKS.json dense bf16 (TF32 at half rate)
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        peak = float(peaks.get("bf16_tflops", 2250.0)) * (0.5 if dom_fam == "tf32" else 1.0)
+        peak_source = ("MEASURED_PEAKS.json bf16_tflops" if peaks else "nominal 2.25 PF/s bf16") + \
+            (" x 1/2 (tf32 rate)" if dom_fam == "tf32" else "")
+    else:
+        peak = gemm.ffma_peak_tflops(packed=True)
+        peak_source = ("measured on this device by kp_ffma_peak (FFMA2 register loop); "
+                       "MEASURED_PEAKS.json has no FP32 SIMT figure")
     achieved = dp.flops / (dom_ms * 1e-3) / 1e12
     traffic = None
     prof = ROOT / "profiles" / "dominant_kernel_traffic.json"
@@ -428,7 +438,8 @@ def run_ours(args, world, rank, local):
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": {"bf16": "bf16", "tf32": "tf32"}.get(args.family, "f32"),
+            "data": "synthetic",
             "config": {"workload": f"vgg16-gemm-layers-b{args.batch}-{args.method}{args.k}-{args.classifier}",
                        "batch_per_gpu": args.batch, "family": args.family, "table": os.path.relpath(args.table, ROOT),
                        "table_shape": [pm.n_problems, pm.n_configs], "parallelism": f"replicas{world}",
@@ -441,14 +452,14 @@ def run_ours(args, world, rank, local):
                           "host_s": sel_t},
             "selection_grid_treeA": selection_grid(pm),
             "gpu_launches": len(bufs) * args.steps,
-            "roofline": {"bound": "compute", "pipe": "fp32 FFMA2 (SIMT)", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes": 4 * (dp.m * dp.k + dp.k * dp.n + dp.m * dp.n),
+            "roofline": {"bound": "tensor" if tensor else "compute",
+                         "pipe": f"tcgen05 {dom_fam}" if tensor else "fp32 FFMA2 (SIMT)", "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes": in_dtype.itemsize * (dp.m * dp.k + dp.k * dp.n) + 4 * dp.m * dp.n,
                          "flops_per_launch": dp.flops, "avg_launch_ms": dom_ms,
                          "kernel": f"{dom_fam}{dom_cfg.as_tuple()} on {dname} {[dp.m, dp.k, dp.n, dp.batch]}",
                          "share_of_step": dg["ms"] / total_ms, "variant_share_of_step": variant_ms / total_ms,
-                         "peak_source": "measured on this device by kp_ffma_peak (FFMA2 register loop); "
-                                        "MEASURED_PEAKS.json has no FP32 SIMT figure"},
+                         "peak_source": peak_source},
             "clocks": clocks.summary(),
         }
         if e2e is not None:
@@ -536,7 +547,8 @@ def run_vgg16_infer(args, world, rank, local):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (He-init weights)",
+                "scaling": "weak", "vs_baseline": None,
+                "dtype": {"bf16": "bf16", "tf32": "tf32"}.get(args.family, "f32"), "data": "synthetic (He-init weights)",
                 "config": {"workload": f"vgg16-infer-b{args.batch}-{args.method}{args.k}-{args.classifier}",
                            "batch_per_gpu": args.batch, "family": args.family, "parallelism": f"dp{world}",
                            "table": os.path.relpath(args.table, ROOT), "cuda_graph": True},
