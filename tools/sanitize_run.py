@@ -1,7 +1,8 @@
 """Small launches of every family / code path for compute-sanitizer (memcheck, racecheck,
 synccheck): F0 and F1 vector + scalar (unaligned) paths, tcgen05 TMA and LSU paths,
-k-sliced cluster launches (F1 and tcgen05: DSMEM slice reduction), the TMA-store
-epilogue, epilogue bias/ReLU, im2col and max-pool."""
+k-sliced cluster launches (F1 and tcgen05: DSMEM slice reduction), the tcgen05
+partial-last-wave split, the TMA-store epilogue, epilogue bias/ReLU, kp_bench_sets,
+im2col (plain, padded, bf16), the bf16 cast and max-pool."""
 import sys
 
 import torch
@@ -30,7 +31,28 @@ for fam, cfg, (m, k, n) in (("simt", KernelConfig(4, 8, 8, 16, 8), (50, 2048, 70
     from paper_2008_13145_b200.dataset import ProblemSize
     assert gemm.k_slice_plan(cfg, ProblemSize(m, k, n, 1), family=fam)[0] > 1, (fam, cfg)
     gemm.matmul(torch.rand(m, k, device=dev).to(dt), torch.rand(k, n, device=dev).to(dt), cfg, fam)
+# tensor-core partial-last-wave split (persistent head + sliced tail launch)
+from paper_2008_13145_b200.dataset import ProblemSize  # noqa: E402
+cfg = gemm.family_configs("tf32")[3]
+assert gemm.k_slice_plan(cfg, ProblemSize(1280, 3456, 4096, 1), family="tf32")[0] > 1
+gemm.matmul(torch.rand(1280, 3456, device=dev), torch.rand(3456, 4096, device=dev), cfg, "tf32")
+# the sweep's rotating / median harness
+ops = [gemm.GemmOperands(torch.rand(40, 64, device=dev), torch.rand(64, 24, device=dev), None, torch.float32)
+       for _ in range(2)]
+gemm.bench_sets(gemm.variant_id(KernelConfig(4, 4, 4, 16, 16), "simt"), ops, warmup=1, min_ms=0.05, repeats=3)
 lib = _lib.load()
+# padded / bf16 im2col and the bf16 cast (VGG16 conv1_1 and the BF16 family)
+xi = torch.rand(2, 6, 6, 3, device=dev)
+pad = torch.empty(72, 28, device=dev)
+_lib.check(lib.kp_im2col3x3_nhwc_pad(xi.data_ptr(), 2, 6, 6, 3, pad.data_ptr(), 28, None), "im2col pad")
+colsb = torch.empty(72, 32, device=dev, dtype=torch.bfloat16)
+_lib.check(lib.kp_im2col3x3_nhwc_bf16(xi.data_ptr(), 2, 6, 6, 3, colsb.data_ptr(), 32, None), "im2col bf16 c3")
+x8 = torch.rand(2, 6, 6, 8, device=dev)
+cols8 = torch.empty(72, 72, device=dev, dtype=torch.bfloat16)
+_lib.check(lib.kp_im2col3x3_nhwc_bf16(x8.data_ptr(), 2, 6, 6, 8, cols8.data_ptr(), 72, None), "im2col bf16 c8")
+v = torch.rand(64, device=dev)
+vb = torch.empty(64, device=dev, dtype=torch.bfloat16)
+_lib.check(lib.kp_cast_bf16(v.data_ptr(), 64, vb.data_ptr(), None), "cast")
 A = torch.rand(70, 64, device=dev)
 W = torch.rand(64, 72, device=dev)
 C = torch.empty(70, 72, device=dev)
