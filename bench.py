@@ -11,12 +11,22 @@ and He-scaled weights of the VGG16 layer shapes; the per-step inputs (~4.3 GB at
 B=16) exceed the 126 MB L2, so no L2 flush is needed between steps.
 
 JSON line keys: value = GFLOP/s of the dispatched step (inputs resident in HBM);
-e2e = the same with host-pinned activations copied H2D and outputs copied D2H inside
-the timed region; roofline = the dominant launch against the measured FP32 FFMA2 peak;
+e2e = the same layer set fed from HOST memory: every step uploads each layer's input
+activation (NHWC, pinned) and reads every layer's output back, with the conv layers'
+im2col done on the device (kp_im2col3x3_nhwc) inside the timed region; roofline = the
+dominant launch against min(pipe peak, arithmetic intensity x HBM bandwidth);
 selection = the north-star metric (geomean fraction of per-shape oracle-best GFLOP/s
 of the k-means subset + tree on the held-out split, evaluate.py:71-101);
-cpu_baseline = the oracle port (oracle/gemm_ref.c fmaf chain, all host threads) on
-a bounded sample (batch 1).  ``--impl reference`` runs that CPU path alone.
+cpu_baseline = np.matmul fp32 (numpy/OpenBLAS, the reference package's numeric
+engine; the reference ships no GEMM) on all host cores over the SAME layer set and
+batch; cpu_port = the bit-exact fmaf-chain oracle port on the same sample.
+``--impl reference`` runs the np.matmul CPU path alone on the same config.
+
+``--gpus N`` without a torchrun environment re-launches this script under
+``torch.distributed.run`` with N ranks; under torchrun WORLD_SIZE must equal N.
+``--workload vgg16-infer`` is BASELINE configs[2] (images/s, data parallel);
+``--workload sweep`` times the sharded benchmark sweep (configs[3], one LPT shard of
+problem rows per rank, no collective) and checks the merged table's canonical order.
 """
 
 from __future__ import annotations
@@ -39,7 +49,8 @@ METRIC = "geomean % of oracle-best GFLOP/s (clustered set + tree); GFLOP/s vs FP
 
 def parse_args(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="GPUs (ranks); default 1, or WORLD_SIZE under torchrun")
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
@@ -49,8 +60,13 @@ def parse_args(argv=None):
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--method", default="kmeans")
     ap.add_argument("--classifier", default="treeA")
-    ap.add_argument("--workload", choices=("gemm-layers", "vgg16-infer"), default="gemm-layers",
-                    help="gemm-layers: BASELINE configs[1] (default); vgg16-infer: configs[2], data parallel")
+    ap.add_argument("--workload", choices=("gemm-layers", "vgg16-infer", "sweep"), default="gemm-layers",
+                    help="gemm-layers: BASELINE configs[1] (default); vgg16-infer: configs[2], data parallel; "
+                         "sweep: the benchmark sweep sharded over the ranks")
+    ap.add_argument("--sweep-set", default="vgg16", help="sweep workload: vgg16 | resnet50 | square")
+    ap.add_argument("--sweep-stride", type=int, default=10,
+                    help="sweep workload: every n-th config of the family (1 = the full table)")
+    ap.add_argument("--sweep-min-ms", type=float, default=1.0, help="sweep workload: timed ms per cell")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args(argv)
@@ -205,85 +221,227 @@ def vgg16_layers(batch: int):
     return out
 
 
-def cpu_baseline(batch: int = 1, repeats: int = 2):
-    """Oracle port (oracle/gemm_ref.c, bit-exact fmaf chain, all host threads) on the
-    VGG16 layer set at ``batch``: GFLOP/s.  TEST INFRASTRUCTURE used as the checker
-    and CPU reference timing only."""
+def _layer_operands(batch: int, seed: int = 0):
     import numpy as np
 
-    from oracle import gemm_oracle as go
-
-    threads = go.set_threads()  # all host CPUs, whatever OMP_NUM_THREADS the launcher set
+    rng = np.random.default_rng(seed)
     layers = vgg16_layers(batch)
-    rng = np.random.default_rng(0)
     ops = [(rng.uniform(-1, 1, (p.m, p.k)).astype(np.float32), rng.uniform(-1, 1, (p.k, p.n)).astype(np.float32))
            for _, p in layers]
-    flops = sum(p.flops for _, p in layers)
-    best = math.inf
-    for _ in range(repeats):
-        t0 = time.perf_counter()
-        for A, B in ops:
-            go.gemm_chain(A, B)
-        best = min(best, time.perf_counter() - t0)
-    return flops / best / 1e9, best, flops, threads
+    return ops, sum(p.flops for _, p in layers)
 
 
-def cpu_blas_line(batch: int = 1, repeats: int = 2):
-    """Strongest CPU comparison: np.matmul fp32 (OpenBLAS, all host threads) on the same
-    bounded sample -- the reference package's numeric engine; reported
-    beside cpu_baseline, never a product path."""
+def cpu_numpy_steps(batch: int, steps: int, warmup: int = 0):
+    """np.matmul fp32 (numpy -> OpenBLAS on every host core) over the VGG16 GEMM layer
+    set at ``batch``: the reference package's numeric engine (SURVEY.md 8(c)/(d) CPU
+    plan; the reference itself ships no GEMM).  Returns (GFLOP/s, per-step seconds,
+    flops per step, cores)."""
     import numpy as np
 
-    layers = vgg16_layers(batch)
-    rng = np.random.default_rng(0)
-    ops = [(rng.uniform(-1, 1, (p.m, p.k)).astype(np.float32), rng.uniform(-1, 1, (p.k, p.n)).astype(np.float32))
-           for _, p in layers]
-    flops = sum(p.flops for _, p in layers)
-    best = math.inf
-    for _ in range(repeats):
+    ops, flops = _layer_operands(batch)
+    secs = []
+    for i in range(warmup + steps):
         t0 = time.perf_counter()
         for A, B in ops:
             np.matmul(A, B)
-        best = min(best, time.perf_counter() - t0)
-    return {"value": flops / best / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "numpy-openblas",
-            "sample": f"VGG16 GEMM layer set at batch {batch} ({flops / 1e9:.2f} GFLOP, best of {repeats}), "
-                      "np.matmul fp32 (not the bit-exact fma chain)"}
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            secs.append(dt)
+    return flops * len(secs) / sum(secs) / 1e9, secs, flops, _blas_threads()
+
+
+def _blas_threads() -> int:
+    """Threads OpenBLAS actually uses (torchrun exports OMP_NUM_THREADS=1, so the
+    reference arm raises it to every host CPU before numpy is imported)."""
+    try:
+        from threadpoolctl import threadpool_info
+        n = [d["num_threads"] for d in threadpool_info() if d.get("internal_api") == "openblas"]
+        if n:
+            return int(n[0])
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+def cpu_port_line(batch: int):
+    """The bit-exact oracle port (oracle/gemm_ref.c fmaf chain, OpenMP over every host
+    CPU) on the same layer set and batch, one pass: TEST INFRASTRUCTURE used as the
+    checker and a second CPU timing only."""
+    from oracle import gemm_oracle as go
+
+    threads = go.set_threads()
+    ops, flops = _layer_operands(batch)
+    t0 = time.perf_counter()
+    for A, B in ops:
+        go.gemm_chain(A, B)
+    dt = time.perf_counter() - t0
+    return {"value": flops / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"VGG16 GEMM layer set at batch {batch} ({flops / 1e9:.1f} GFLOP, one pass), "
+                      "oracle/gemm_ref.c bit-exact fmaf chain, OpenMP over rows"}
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the CPU path (oracle port) on the host cores; rank 0 only."""
+    """--impl reference: the CPU path on the host cores, rank 0 only, SAME config as the
+    GPU arm (VGG16 GEMM layer set at --batch): np.matmul fp32 on every host core."""
     if rank != 0:
         return 0
-    sample_batch = 1
-    gf, secs, flops = None, [], 0
-    from oracle import gemm_oracle as go
-    import numpy as np
-    cores = go.set_threads()  # torchrun exports OMP_NUM_THREADS=1; use every host CPU
-    layers = vgg16_layers(sample_batch)
-    rng = np.random.default_rng(0)
-    ops = [(rng.uniform(-1, 1, (p.m, p.k)).astype(np.float32), rng.uniform(-1, 1, (p.k, p.n)).astype(np.float32))
-           for _, p in layers]
-    flops = sum(p.flops for _, p in layers)
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        for A, B in ops:
-            go.gemm_chain(A, B)
-        dt = time.perf_counter() - t0
-        if i >= args.warmup:
-            secs.append(dt)
-    total = sum(secs)
-    gf = flops * len(secs) / total / 1e9
-    sample = (f"VGG16 GEMM layer set at batch {sample_batch} ({flops / 1e9:.2f} GFLOP/step) instead of batch "
-              f"{args.batch}; oracle/gemm_ref.c fmaf chain, OpenMP over rows")
-    line = {"metric": METRIC, "value": gf, "unit": "GFLOP/s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / len(secs) * 1e3,
+    gf, secs, flops, cores = cpu_numpy_steps(args.batch, args.steps, args.warmup)
+    sample = (f"the full VGG16 GEMM layer set at batch {args.batch} ({flops / 1e9:.1f} GFLOP/step, "
+              f"{len(secs)} steps after {args.warmup} warm-up), np.matmul fp32 -> OpenBLAS")
+    line = {"metric": METRIC, "value": gf, "unit": "GFLOP/s", "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(secs) / len(secs) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"vgg16-gemm-layers-b{args.batch}-kmeans{args.k}-{args.classifier}",
-                       "batch": args.batch},
-            "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample},
+            "config": {"workload": f"vgg16-gemm-layers-b{args.batch}-{args.method}{args.k}-{args.classifier}",
+                       "batch_per_gpu": args.batch, "same_config_as_gpu_arm": True},
+            "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+                             "sample": sample,
+                             "note": "the reference package has no GEMM; numpy (its only numeric engine) is "
+                                     "the CPU path it would call"},
             "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ----------------------------------------------------------------- roofline --
+def measured_peaks() -> dict:
+    path = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return json.loads(path.read_text()) if path.exists() else {}
+    except Exception:
+        return {}
+
+
+def roofline(family: str, p, ms: float, in_bytes: int, simt_peak: float | None = None) -> dict:
+    """Roofline of one launch: attainable = min(pipe peak, AI x HBM bandwidth) with the
+    algorithmic bytes in_bytes*(mk + kn) + 4*mn; the binding term
+    decides whether the launch is reported in TFLOP/s or GB/s."""
+    from paper_2008_13145_b200 import gemm
+
+    peaks = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 0.0)) or 7700.0
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "nominal 7.7 TB/s (no MEASURED_PEAKS.json)"
+    if family in ("tf32", "bf16"):
+        pipe = float(peaks.get("bf16_tflops", 0.0)) or 2250.0
+        pipe_src = "MEASURED_PEAKS.json bf16_tflops" if peaks.get("bf16_tflops") else "nominal 2.25 PF/s bf16"
+        if family == "tf32":
+            pipe, pipe_src = pipe / 2, pipe_src + " x 1/2 (tf32 rate)"
+        pipe_name = f"tcgen05 {family}"
+    else:
+        pipe = simt_peak if simt_peak is not None else gemm.ffma_peak_tflops(packed=True)
+        pipe_src = "kp_ffma_peak on this device (FFMA2 register loop; MEASURED_PEAKS.json has no FP32 figure)"
+        pipe_name = "fp32 FFMA2 (SIMT)"
+    flops = p.flops
+    nbytes = p.batch * (in_bytes * (p.m * p.k + p.k * p.n) + 4 * p.m * p.n)
+    ai = flops / nbytes
+    sec = ms * 1e-3
+    if ai * hbm / 1e3 < pipe:  # HBM-bound: AI x BW (GB/s -> TFLOP/s) is the lower roof
+        return {"bound": "hbm", "achieved": nbytes / sec / 1e9, "peak": hbm, "unit": "GB/s",
+                "frac": nbytes / sec / 1e9 / hbm, "pipe": pipe_name, "peak_source": hbm_src,
+                "algorithmic_bytes": nbytes, "flops_per_launch": flops, "arith_intensity": ai,
+                "achieved_tflops": flops / sec / 1e12}
+    return {"bound": "tensor" if family in ("tf32", "bf16") else "compute", "achieved": flops / sec / 1e12,
+            "peak": pipe, "unit": "TFLOP/s", "frac": flops / sec / 1e12 / pipe, "pipe": pipe_name,
+            "peak_source": pipe_src, "algorithmic_bytes": nbytes, "flops_per_launch": flops, "arith_intensity": ai,
+            "hbm_roof_tflops": ai * hbm / 1e3}
+
+
+# ---------------------------------------------------------------------- e2e --
+def e2e_layers(args, world, device, stream, disp, bufs, step_flops, in_dtype):
+    """The layer set through the public API from HOST memory: every step uploads each
+    layer's input activation from pinned memory -- NHWC (B, H, W, Cin) for the conv
+    layers, (B, k) rows for fc -- lowers the conv ones on the device (kp_im2col3x3_nhwc,
+    + kp_cast_bf16 for the BF16 family), runs the dispatched GEMM and copies every
+    layer's output back to pinned memory.  Uploads run on one copy stream, downloads on
+    another, overlapping the compute stream layer by layer.  FLOPs counted are the GEMMs'
+    only (im2col is extra work inside the timed region)."""
+    import torch
+
+    from paper_2008_13145_b200 import _lib, shapes
+
+    lib = _lib.load()
+    geo = {}
+    for layer in shapes.VGG16_LAYERS:
+        geo[layer.name] = None if layer.fc else (math.isqrt(layer.m_per_image), layer.k // 9)
+    names = []
+    for layer in shapes.VGG16_LAYERS:
+        names += [layer.name] * layer.count
+    gen = torch.Generator().manual_seed(99)
+    host_in, dev_in, scratch = [], [], {}
+    for (name, p, A, W, C, vid), lname in zip(bufs, names):
+        g = geo[lname]
+        shape = (args.batch, g[0], g[0], g[1]) if g else (p.m, p.k)
+        h = (torch.rand(shape, generator=gen) * 2 - 1).pin_memory()
+        host_in.append(h)
+        dev_in.append(torch.empty(shape, device=device))
+    host_out = [torch.empty(C.shape, dtype=C.dtype, pin_memory=True) for *_, C, _ in bufs]
+    h2d = sum(t.numel() * t.element_size() for t in host_in)
+    d2h = sum(t.numel() * t.element_size() for t in host_out)
+    bf16 = in_dtype == torch.bfloat16
+    if bf16:
+        biggest = max(p.m * p.k for _, p, *_ in bufs)
+        scratch = torch.empty(biggest, device=device)
+    h2d_stream, d2h_stream = torch.cuda.Stream(device), torch.cuda.Stream(device)
+    landed = [torch.cuda.Event() for _ in bufs]
+    computed = [torch.cuda.Event() for _ in bufs]
+    s_handle = stream.cuda_stream
+    launches = [0]
+
+    def lower(i, lname, p, A):
+        """Device-side operand for layer i: im2col (conv) / cast (bf16) into A."""
+        g = geo[lname]
+        x = dev_in[i]
+        if g is None and not bf16:
+            return x
+        target = scratch if bf16 else A
+        if g is not None:
+            _lib.check(lib.kp_im2col3x3_nhwc(x.data_ptr(), args.batch, g[0], g[0], g[1], target.data_ptr(), p.k,
+                                             s_handle), "kp_im2col3x3_nhwc")
+            launches[0] += 1
+            src = target
+        else:
+            src = x
+        if bf16:
+            _lib.check(lib.kp_cast_bf16(src.data_ptr(), p.m * p.k, A.data_ptr(), s_handle), "kp_cast_bf16")
+            launches[0] += 1
+        return A
+
+    def e2e_step():
+        with torch.cuda.stream(h2d_stream):
+            for i in range(len(bufs)):
+                dev_in[i].copy_(host_in[i], non_blocking=True)
+                landed[i].record(h2d_stream)
+        for i, ((name, p, A, W, C, vid), lname) in enumerate(zip(bufs, names)):
+            stream.wait_event(landed[i])
+            operand = lower(i, lname, p, A)
+            disp.matmul(operand.view(p.m, p.k), W, out=C, stream=stream)
+            launches[0] += 1
+            computed[i].record(stream)
+            d2h_stream.wait_event(computed[i])
+            with torch.cuda.stream(d2h_stream):
+                host_out[i].copy_(C, non_blocking=True)
+        stream.wait_stream(d2h_stream)
+        h2d_stream.wait_stream(stream)  # the next step's uploads may not overwrite inputs in use
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+    torch.cuda.synchronize(device)
+    barrier(world)
+    launches[0] = 0
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        f0.record(stream)
+        h2d_stream.wait_stream(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        f1.record(stream)
+    torch.cuda.synchronize(device)
+    e2e_ms = reduce_max(f0.elapsed_time(f1), world, device)
+    return {"value": step_flops * args.steps * world / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
+            "launches_per_step": launches[0] // args.steps,
+            "path": "host NHWC activations -> H2D -> kp_im2col3x3_nhwc" + (" + kp_cast_bf16" if bf16 else "")
+                    + " -> Dispatcher.matmul (kp_gemm) -> D2H of every layer output"}
 
 
 # ---------------------------------------------------------------------- ours --
@@ -356,83 +514,31 @@ def run_ours(args, world, rank, local):
     dom_ms = dg["ms"] / dg["launches"]
     dom_cfg, dom_fam = gemm.variant_info(dvid)
     dname = "+".join(dg["names"])
-    tensor = dom_fam in ("tf32", "bf16")
-    if tensor:  # tensor-pipe roofline: MEASURED_PEAKS.json dense bf16 (TF32 at half rate)
-        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-        peak = float(peaks.get("bf16_tflops", 2250.0)) * (0.5 if dom_fam == "tf32" else 1.0)
-        peak_source = ("MEASURED_PEAKS.json bf16_tflops" if peaks else "nominal 2.25 PF/s bf16") + \
-            (" x 1/2 (tf32 rate)" if dom_fam == "tf32" else "")
-    else:
-        peak = gemm.ffma_peak_tflops(packed=True)
-        peak_source = ("measured on this device by kp_ffma_peak (FFMA2 register loop); "
-                       "MEASURED_PEAKS.json has no FP32 SIMT figure")
-    achieved = dp.flops / (dom_ms * 1e-3) / 1e12
+    roof = roofline(dom_fam, dp, dom_ms, in_dtype.itemsize)
     traffic = None
     prof = ROOT / "profiles" / "dominant_kernel_traffic.json"
     if prof.exists():
         try:
             rec = json.loads(prof.read_text())
             for r in rec.get("launches", [rec]):
-                if r.get("variant") == list(dom_cfg.as_tuple()) and r.get("problem") == [dp.m, dp.k, dp.n, dp.batch]:
+                if (r.get("family", "simt") == dom_fam and r.get("variant") == list(dom_cfg.as_tuple())
+                        and r.get("problem") == [dp.m, dp.k, dp.n, dp.batch]):
                     traffic = r.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    roof["traffic"] = traffic
     total_ms = sum(layer_ms)
 
-    # e2e: host-pinned activations in, outputs out, through the dispatcher
-    e2e = None
-    if not args.no_e2e:
-        host_in = [A.cpu().pin_memory() for _, _, A, _, _, _ in bufs]
-        host_out = [torch.empty(C.shape, dtype=C.dtype, pin_memory=True) for _, _, _, _, C, _ in bufs]
-        dev_in = [torch.empty_like(A) for _, _, A, _, _, _ in bufs]
-        h2d = sum(t.numel() * t.element_size() for t in host_in)
-        d2h = sum(t.numel() * t.element_size() for t in host_out)
+    e2e = None if args.no_e2e else e2e_layers(args, world, device, stream, disp, bufs, step_flops, in_dtype)
 
-        # three-stage pipeline over the layers: H2D of layer i+1 (copy stream) and D2H
-        # of layer i-1 (second copy engine) overlap the GEMM of layer i (compute stream)
-        h2d_stream, d2h_stream = torch.cuda.Stream(device), torch.cuda.Stream(device)
-        landed = [torch.cuda.Event() for _ in bufs]
-        computed = [torch.cuda.Event() for _ in bufs]
-
-        def e2e_step():
-            for i, (name, p, A, W, C, vid) in enumerate(bufs):
-                with torch.cuda.stream(h2d_stream):
-                    dev_in[i].copy_(host_in[i], non_blocking=True)
-                    landed[i].record(h2d_stream)
-            for i, (name, p, A, W, C, vid) in enumerate(bufs):
-                stream.wait_event(landed[i])
-                disp.matmul(dev_in[i], W, out=C, stream=stream)
-                computed[i].record(stream)
-                d2h_stream.wait_event(computed[i])
-                with torch.cuda.stream(d2h_stream):
-                    host_out[i].copy_(C, non_blocking=True)
-            stream.wait_stream(d2h_stream)
-            h2d_stream.wait_stream(stream)  # next step's H2D may not overwrite inputs in use
-
-        with torch.cuda.stream(stream):
-            for _ in range(max(1, args.warmup)):
-                e2e_step()
-        torch.cuda.synchronize(device)
-        barrier(world)
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            f0.record(stream)
-            h2d_stream.wait_stream(stream)
-            for _ in range(args.steps):
-                e2e_step()
-            f1.record(stream)
-        torch.cuda.synchronize(device)
-        e2e_ms = reduce_max(f0.elapsed_time(f1), world, device)
-        e2e = {"value": step_flops * args.steps * world / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps}
-
-    cpu = cpu_blas = None
+    cpu = cpu_port = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        gf, secs, flops, threads = cpu_baseline(batch=1)
-        cpu = {"value": gf, "unit": "GFLOP/s", "cores": threads, "kind": "port",
-               "sample": f"VGG16 GEMM layer set at batch 1 ({flops / 1e9:.2f} GFLOP, best of 2) with "
-                         f"oracle/gemm_ref.c (bit-exact fmaf chain, OpenMP all threads)"}
-        cpu_blas = cpu_blas_line(batch=1)
+        gf, secs, flops, cores = cpu_numpy_steps(args.batch, steps=1, warmup=1)
+        cpu = {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+               "sample": f"the same VGG16 GEMM layer set at batch {args.batch} ({flops / 1e9:.1f} GFLOP, one step "
+                         "after one warm-up), np.matmul fp32 -> OpenBLAS (the reference package's numeric engine; "
+                         "it ships no GEMM)"}
+        cpu_port = cpu_port_line(args.batch)
 
     if rank == 0:
         line = {
@@ -444,7 +550,7 @@ def run_ours(args, world, rank, local):
                        "batch_per_gpu": args.batch, "family": args.family, "table": os.path.relpath(args.table, ROOT),
                        "table_shape": [pm.n_problems, pm.n_configs], "parallelism": f"replicas{world}",
                        "l2": "per-step inputs ~%.1f GB > 126 MB L2 (no flush needed)" %
-                             (sum(A.numel() * 4 for _, _, A, _, _, _ in bufs) / 1e9)},
+                             (sum(A.numel() * A.element_size() for _, _, A, _, _, _ in bufs) / 1e9)},
             "selection": {"method": args.method, "k": args.k, "classifier": args.classifier,
                           "subset": [list(pm.configs[i].as_tuple()) for i in subset.config_indices],
                           "achieved_test": rep_test.achieved, "ceiling_test": rep_test.ceiling,
@@ -452,21 +558,17 @@ def run_ours(args, world, rank, local):
                           "host_s": sel_t},
             "selection_grid_treeA": selection_grid(pm),
             "gpu_launches": len(bufs) * args.steps,
-            "roofline": {"bound": "tensor" if tensor else "compute",
-                         "pipe": f"tcgen05 {dom_fam}" if tensor else "fp32 FFMA2 (SIMT)", "achieved": achieved,
-                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes": in_dtype.itemsize * (dp.m * dp.k + dp.k * dp.n) + 4 * dp.m * dp.n,
-                         "flops_per_launch": dp.flops, "avg_launch_ms": dom_ms,
-                         "kernel": f"{dom_fam}{dom_cfg.as_tuple()} on {dname} {[dp.m, dp.k, dp.n, dp.batch]}",
-                         "share_of_step": dg["ms"] / total_ms, "variant_share_of_step": variant_ms / total_ms,
-                         "peak_source": peak_source},
+            "gpu_launches_e2e": e2e["launches_per_step"] * args.steps if e2e else None,
+            "roofline": dict(roof, kernel=f"{dom_fam}{dom_cfg.as_tuple()} on {dname} {[dp.m, dp.k, dp.n, dp.batch]}",
+                             avg_launch_ms=dom_ms, share_of_step=dg["ms"] / total_ms,
+                             variant_share_of_step=variant_ms / total_ms),
             "clocks": clocks.summary(),
         }
         if e2e is not None:
             line["e2e"] = e2e
         if cpu is not None:
             line["cpu_baseline"] = cpu
-            line["cpu_blas"] = cpu_blas
+            line["cpu_port"] = cpu_port
         print(json.dumps(line), flush=True)
     return 0
 
@@ -562,14 +664,128 @@ def run_vgg16_infer(args, world, rank, local):
     return 0
 
 
+def run_sweep(args, world, rank, local):
+    """BASELINE configs[3]-style sweep scaling: the benchmark sweep of ``--sweep-set``
+    over every ``--sweep-stride``-th config of ``--family``, problem rows sharded across
+    the ranks by LPT (sweep.lpt_shards; no collective on the data path), each rank
+    measuring its shard on its own GPU into a partial CSV.  Rank 0 merges canonically
+    and asserts the row / column order.  value = table cells per second over the whole
+    job (strong scaling: the table is fixed, more ranks finish it sooner); the time is
+    each rank's shard bracketed by CUDA events on its timer stream, max over ranks."""
+    import tempfile
+
+    import torch
+
+    from paper_2008_13145_b200 import gemm, sweep
+
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    problems = sweep.problem_set(args.sweep_set)
+    all_cfgs = gemm.family_configs(args.family)
+    cols = list(range(0, len(all_cfgs), max(1, args.sweep_stride)))
+    cfgs = tuple(all_cfgs[c] for c in cols)
+    shards = sweep.lpt_shards(problems, world)
+    mine = shards[rank]
+    timer = sweep.CudaEventTimer(args.family, [problems[r] for r in mine] or problems[:1], device=local,
+                                 min_ms=args.sweep_min_ms)
+
+    class Columns:  # the strided config subset as a timer over local column indices
+        configs = cfgs
+
+        def __call__(self, problem, ci):
+            return timer(problem, cols[ci])
+
+        def conditions(self):
+            return timer.conditions()
+
+    work = Path(os.environ.get("KP_BENCH_SWEEP_DIR") or
+                Path(tempfile.gettempdir()) / f"kp_bench_sweep_{os.environ.get('MASTER_PORT', os.getpid())}")
+    work.mkdir(parents=True, exist_ok=True)
+    part = work / f"shard{rank}.csv"
+    for w in range(args.warmup):  # warm-up: one cell per rank (module load, clocks)
+        timer(problems[mine[0] if mine else 0], cols[w % len(cols)])
+    torch.cuda.synchronize(device)
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record(timer.stream)
+        total_ms = 0.0
+        for s in range(args.steps):
+            if part.exists():
+                part.unlink()  # each step re-measures the shard from scratch
+            sweep.run_shard(problems, mine, len(cfgs), Columns(), part)
+        e1.record(timer.stream)
+        torch.cuda.synchronize(device)
+        total_ms = e0.elapsed_time(e1)
+    ms = reduce_max(total_ms, world, device)
+    barrier(world)
+    if rank != 0:
+        return 0
+    cells = {}
+    for r in range(world):
+        if shards[r]:
+            cells.update(sweep._read_partial(work / f"shard{r}.csv"))
+    pm = sweep.merge_cells(problems, cfgs, cells)
+    assert list(pm.problems) == list(problems) and list(pm.configs) == list(cfgs), "merge is not canonical"
+    n_cells = len(problems) * len(cfgs)
+    flops = sum(p.flops for p in problems) * len(cfgs)
+    line = {"metric": METRIC, "value": n_cells * args.steps / (ms * 1e-3), "unit": "cells/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": {"bf16": "bf16", "tf32": "tf32"}.get(args.family, "f32"),
+            "data": "synthetic",
+            "config": {"workload": f"sweep-{args.sweep_set}-{args.family}-stride{args.sweep_stride}",
+                       "table_shape": [len(problems), len(cfgs)], "min_ms_per_cell": args.sweep_min_ms,
+                       "parallelism": f"lpt-shards{world}", "l2": "operands rotated over >= 2 x L2 per cell"},
+            "shard_rows": [len(sh) for sh in shards], "merged_canonical": True,
+            "timed_gflop_per_step": flops / 1e9, "clocks": clocks.summary(),
+            "gpu_launches": None}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def self_launch(args, argv) -> int | None:
+    """--gpus N outside torchrun: re-run this script under torch.distributed.run with N
+    ranks (127.0.0.1 rendezvous) and return its exit code; None when no launch is
+    needed.  Under torchrun, WORLD_SIZE must match --gpus."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None:
+        if args.gpus is not None and int(env_world) != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}")
+        return None
+    if (args.gpus or 1) <= 1:
+        return None
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+           *(argv if argv is not None else sys.argv[1:])]
+    return subprocess.call(cmd)
+
+
 def main(argv=None):
     args = parse_args(argv)
+    rc = self_launch(args, argv)
+    if rc is not None:
+        return rc
+    if args.impl == "reference":
+        # torchrun exports OMP_NUM_THREADS=1; the CPU arm uses every host core
+        n = str(os.cpu_count() or 1)
+        os.environ["OMP_NUM_THREADS"] = n
+        os.environ["OPENBLAS_NUM_THREADS"] = n
     world, rank, local = dist_setup(args)
+    if args.gpus is None:
+        args.gpus = world
     try:
         if args.impl == "reference":
             return run_reference(args, world, rank)
         if args.workload == "vgg16-infer":
             return run_vgg16_infer(args, world, rank, local)
+        if args.workload == "sweep":
+            return run_sweep(args, world, rank, local)
         return run_ours(args, world, rank, local)
     finally:
         import torch.distributed as dist

@@ -160,8 +160,9 @@ int kp_ffma_peak(int packed, double* tflops, void* stream);
  * A flattened CART tree in preorder (classify.py:56-77): internal nodes carry
  * feature in [0,4) and threshold; leaves carry leaf_class >= 0.  class_to_variant
  * maps the subset-local class (label_best_in_subset, classify.py:32-34) to a
- * variant id.  Returns a table handle >= 0.  Loading is not concurrent with
- * selection on the same handle; selection is reentrant. */
+ * variant id.  Returns a table handle >= 0.  Tables are immutable once loaded; load,
+ * free and selection are thread-safe (a walk holds its table alive even if another
+ * thread frees the handle meanwhile). */
 int kp_dispatch_load(int n_nodes, const int32_t* feature, const double* threshold,
                      const int32_t* left, const int32_t* right, const int32_t* leaf_class,
                      int n_classes, const int32_t* class_to_variant);

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -294,18 +295,20 @@ kp::GemmArgs make_args(int m, int k, int n, int batch, const void* A, int64_t ld
 }
 
 // ---------------------------------------------------------- dispatch tables --
+// Tables are immutable once loaded and held by shared_ptr: a lookup copies the pointer
+// under the lock, so a concurrent load (vector growth) or free cannot invalidate a walk
+// already in progress.
 struct Table {
-  bool live = false;
   std::vector<int32_t> feature, left, right, leaf_class, class_to_variant;
   std::vector<double> threshold;
 };
 std::mutex g_tables_mu;
-std::vector<Table> g_tables;
+std::vector<std::shared_ptr<const Table>> g_tables;
 
-const Table* get_table(int handle) {
+std::shared_ptr<const Table> get_table(int handle) {
   std::lock_guard<std::mutex> lock(g_tables_mu);
-  if (handle < 0 || handle >= static_cast<int>(g_tables.size()) || !g_tables[handle].live) return nullptr;
-  return &g_tables[handle];
+  if (handle < 0 || handle >= static_cast<int>(g_tables.size())) return nullptr;
+  return g_tables[handle];
 }
 
 // predict_tree (classify.py:230-237): left iff x[f] < thr, strictly.
@@ -583,8 +586,8 @@ int kp_dispatch_load(int n_nodes, const int32_t* feature, const double* threshol
     }
   }
   if (visited != n_nodes) return fail(KP_EINVAL, "unreachable nodes in tree");
-  Table t;
-  t.live = true;
+  auto tp = std::make_shared<Table>();
+  Table& t = *tp;
   t.feature.assign(feature, feature + n_nodes);
   t.threshold.assign(threshold, threshold + n_nodes);
   t.left.assign(left, left + n_nodes);
@@ -592,29 +595,32 @@ int kp_dispatch_load(int n_nodes, const int32_t* feature, const double* threshol
   t.leaf_class.assign(leaf_class, leaf_class + n_nodes);
   t.class_to_variant.assign(class_to_variant, class_to_variant + n_classes);
   std::lock_guard<std::mutex> lock(g_tables_mu);
-  g_tables.push_back(std::move(t));
+  g_tables.push_back(std::move(tp));
   return static_cast<int>(g_tables.size()) - 1;
 }
 
 int kp_dispatch_free(int handle) {
   std::lock_guard<std::mutex> lock(g_tables_mu);
-  if (handle < 0 || handle >= static_cast<int>(g_tables.size()) || !g_tables[handle].live)
+  if (handle < 0 || handle >= static_cast<int>(g_tables.size()) || !g_tables[handle])
     return fail(KP_ENOENT, "unknown dispatch table %d", handle);
-  g_tables[handle] = Table{};
+  g_tables[handle].reset();  // walks holding the table keep it alive until they return
   return KP_OK;
 }
 
 int kp_dispatch_class_feats(int handle, const double* feats4) {
-  const Table* t = get_table(handle);
+  const std::shared_ptr<const Table> t = get_table(handle);
   if (!t) return fail(KP_ENOENT, "unknown dispatch table %d", handle);
   if (!feats4) return fail(KP_EINVAL, "null feature vector");
   return walk(*t, feats4);
 }
 
 int kp_dispatch_select_feats(int handle, const double* feats4) {
-  const int cls = kp_dispatch_class_feats(handle, feats4);
+  const std::shared_ptr<const Table> t = get_table(handle);  // one lookup for class and variant
+  if (!t) return fail(KP_ENOENT, "unknown dispatch table %d", handle);
+  if (!feats4) return fail(KP_EINVAL, "null feature vector");
+  const int cls = walk(*t, feats4);
   if (cls < 0) return cls;
-  return get_table(handle)->class_to_variant[cls];
+  return t->class_to_variant[cls];
 }
 
 int kp_dispatch_select(int handle, int m, int k, int n, int batch) {

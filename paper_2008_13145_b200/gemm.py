@@ -113,10 +113,20 @@ class GemmOperands:
         if B3.shape[1] != k:
             raise ValueError(f"inner dimensions differ: A is (.., {m}, {k}), B is (.., {B3.shape[1]}, {B3.shape[2]})")
         n = B3.shape[2]
+        if A.device != B.device:
+            raise ValueError(f"A is on {A.device} but B is on {B.device}")
         if out is None:
             out = torch.empty((batch, m, n), device=A.device, dtype=torch.float32)
-        elif out.dtype != torch.float32 or tuple(out.shape[-2:]) != (m, n) or out.stride(-1) != 1:
-            raise ValueError("out must be float32 (.., m, n) with contiguous rows")
+        else:
+            if not out.is_cuda or out.device != A.device:
+                raise ValueError(f"out must be a CUDA tensor on {A.device}, got {out.device}")
+            if out.dtype != torch.float32 or out.dim() not in (2, 3) or tuple(out.shape[-2:]) != (m, n) \
+                    or out.stride(-1) != 1:
+                raise ValueError("out must be float32 (m, n) or (batch, m, n) with contiguous rows")
+            if out.dim() == 3 and out.shape[0] != batch:
+                raise ValueError(f"out batch {out.shape[0]} != operand batch {batch}")
+            if out.dim() == 2 and batch > 1:
+                raise ValueError(f"a batched product (batch {batch}) needs a 3-D out")
         C3 = out if out.dim() == 3 else out.unsqueeze(0)
         self.A, self.B, self.C = A3, B3, C3
         self.m, self.k, self.n, self.batch = m, k, n, batch

@@ -12,8 +12,9 @@ SynthModel, dataset.py:147-170) used to test sharding and the canonical merge
 without a GPU.
 
 Multi-GPU: the sweep is embarrassingly parallel.  Problem rows are sharded across
-G worker processes (one per GPU, pinned with CUDA_VISIBLE_DEVICES) by
-longest-processing-time on estimated flops; there is no collective.  Each worker
+G worker processes -- one ``multiprocessing.Process`` per non-empty shard, its GPU
+fixed with CUDA_VISIBLE_DEVICES at spawn (mapped through the parent's own device
+list) -- by longest-processing-time on estimated flops; there is no collective.  Each worker
 writes its shard as a partial CSV (resumable: cells already present are skipped)
 and the parent merges in canonical order -- problem-list order x config order --
 so the table (and hence the k-means seed path, SURVEY.md section 7 hard part 8) is
@@ -248,17 +249,30 @@ def merge_cells(problems, configs, cells) -> PerfMatrix:
     return PerfMatrix(tuple(problems), tuple(configs), table)
 
 
-def _worker(args):
-    (gpu, problems, rows, family, partial, timer_kind, timer_kw) = args
-    os.environ["CUDA_VISIBLE_DEVICES"] = str(gpu)
+def device_bindings(gpus: int) -> list[str]:
+    """CUDA_VISIBLE_DEVICES value for each of ``gpus`` workers: the parent's own device
+    list (a job given GPUs 4-7 by its scheduler sweeps 4-7), else 0..gpus-1."""
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis is None or vis.strip() == "":
+        return [str(g) for g in range(gpus)]
+    devs = [v.strip() for v in vis.split(",") if v.strip()]
+    if len(devs) < gpus:
+        raise ValueError(f"--gpus {gpus} but CUDA_VISIBLE_DEVICES lists only {len(devs)} devices ({vis})")
+    return devs[:gpus]
+
+
+def _worker(gpu_env, problems, rows, family, partial, timer_kind, timer_kw):
+    # The binding is fixed before anything touches CUDA in this fresh (spawned) process,
+    # and each process measures exactly one shard, so no shard can inherit another's GPU.
+    os.environ["CUDA_VISIBLE_DEVICES"] = gpu_env
+    Path(partial).with_suffix(".device").write_text(f"{gpu_env} {os.getpid()}\n")
     if timer_kind == "cuda":
-        timer = CudaEventTimer(family, [problems[r] for r in rows] or problems[:1], **timer_kw)
+        timer = CudaEventTimer(family, [problems[r] for r in rows], **timer_kw)
         n_configs = len(timer.configs)
     else:
         timer = SynthTimer(**timer_kw)
         n_configs = len(timer.configs)
     run_shard(problems, rows, n_configs, timer, Path(partial))
-    return gpu
 
 
 def benchmark_sweep(problems, family: str = "simt", gpus: int = 1, out_dir: str | os.PathLike | None = None,
@@ -290,15 +304,28 @@ def benchmark_sweep(problems, family: str = "simt", gpus: int = 1, out_dir: str 
     if out is None:
         raise ValueError("multi-GPU sweeps need out_dir for the shard files")
     shards = lpt_shards(problems, gpus)
-    jobs = [(g, problems, shards[g], family, str(out / f"shard{g}.csv"), timer_kind, timer_kw)
-            for g in range(gpus)]
+    bindings = device_bindings(gpus)
     ctx = mp.get_context("spawn")
-    with ctx.Pool(gpus) as pool:
-        for _ in pool.imap_unordered(_worker, jobs):
-            pass
+    procs = []
+    for g in range(gpus):
+        if not shards[g]:
+            continue  # more GPUs than problem rows: no worker, no CUDA context
+        proc = ctx.Process(target=_worker, name=f"sweep-gpu{g}",
+                           args=(bindings[g], problems, shards[g], family, str(out / f"shard{g}.csv"),
+                                 timer_kind, timer_kw))
+        proc.start()
+        procs.append(proc)
+    failed = []
+    for proc in procs:
+        proc.join()
+        if proc.exitcode != 0:
+            failed.append(f"{proc.name} exit {proc.exitcode}")
+    if failed:
+        raise RuntimeError("sweep workers failed: " + ", ".join(failed))
     cells: dict = {}
     for g in range(gpus):
-        cells.update(_read_partial(out / f"shard{g}.csv"))
+        if shards[g]:
+            cells.update(_read_partial(out / f"shard{g}.csv"))
     if configs is None:
         if timer_kind == "synth":
             configs = timer_kw["configs"]

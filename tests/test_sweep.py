@@ -105,3 +105,35 @@ def test_cli_sweep_usage_and_config_keys(tmp_path, capsys):
     bad = tmp_path / "cfg.json"
     bad.write_text(json.dumps({"sweep_sets": "vgg16"}))
     assert cli.main(["run", "--config", str(bad), "--output-dir", str(tmp_path / "o")]) == 2
+
+
+def test_multi_gpu_sweep_binds_one_distinct_device_per_shard(tmp_path, monkeypatch):
+    """One process per non-empty shard, each pinned at spawn to its own device of the
+    parent's CUDA_VISIBLE_DEVICES list (here '4,5,6': a scheduler-assigned range)."""
+    monkeypatch.setenv("CUDA_VISIBLE_DEVICES", "4,5,6")
+    probs = PROBS[:2]  # 3 GPUs, 2 rows: one shard is empty and gets no worker
+    par = sweep.benchmark_sweep(probs, gpus=3, out_dir=tmp_path, timer_kind="synth",
+                                timer_kw={"configs": CFGS, "model": SynthModel()}, configs=CFGS)
+    assert par == synth_generate(SynthModel(), probs, list(CFGS))
+    bindings = {}
+    for g in range(3):
+        f = tmp_path / f"shard{g}.device"
+        if f.exists():
+            dev, pid = f.read_text().split()
+            bindings[g] = (dev, int(pid))
+    assert len(bindings) == 2  # the empty shard started nothing
+    devs = [d for d, _ in bindings.values()]
+    pids = [p for _, p in bindings.values()]
+    assert len(set(devs)) == 2 and set(devs) <= {"4", "5", "6"}
+    assert len(set(pids)) == 2
+    for g, (dev, _) in bindings.items():
+        assert dev == "456"[g]
+
+
+def test_device_bindings_respect_parent_mask(monkeypatch):
+    monkeypatch.delenv("CUDA_VISIBLE_DEVICES", raising=False)
+    assert sweep.device_bindings(3) == ["0", "1", "2"]
+    monkeypatch.setenv("CUDA_VISIBLE_DEVICES", "GPU-a, GPU-b")
+    assert sweep.device_bindings(2) == ["GPU-a", "GPU-b"]
+    with pytest.raises(ValueError):
+        sweep.device_bindings(3)
