@@ -25,10 +25,14 @@ LIB_DIR = ROOT / "paper_2008_13145_b200"
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 
 # INTEGRATION.md section 2a, verbatim (test_integration_doc_quotes_this_code checks it)
-RUN_GEMM = r'''#include "kpgemm.h"            /* defines KernelChoice with the emitted field order */
+RUN_GEMM = r'''#include <cuda_runtime.h>
+#include "kpgemm.h"            /* defines KernelChoice with the emitted field order */
 #include "select_kernel.inc"   /* kernelprune codegen output, unchanged */
 #include <math.h>
 
+#ifdef __cplusplus
+extern "C"                     /* C linkage when built as CUDA/C++ host code */
+#endif
 int run_gemm(int m, int k, int n, const float* A, const float* B, float* C, cudaStream_t s) {
   KernelChoice ch = select_kernel(log2(m), log2(k), log2(n), log2(1.0));
   int id = kp_find_variant(KP_FAMILY_SIMT, ch);          /* 5-tuple -> variant id */
@@ -105,11 +109,16 @@ def test_emitted_selector_compiles_and_agrees_with_predict_tree(selector):
 def test_emitted_selector_compiles_as_cuda_host_code(selector):
     *_, work = selector
     (work / "run_gemm.cu").write_text(RUN_GEMM)
+    (work / "run_gemm.c").write_text(RUN_GEMM)
+    cuda_inc = Path(NVCC).resolve().parent.parent / "include"
+    subprocess.run(["gcc", "-std=c99", "-c", "-Wall", "-Werror", f"-I{cuda_inc}", f"-I{ROOT / 'include'}", f"-I{work}",
+                    str(work / "run_gemm.c"), "-o", str(work / "run_gemm_c.o")], check=True, capture_output=True)
     subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC", "-shared",
                     f"-I{ROOT / 'include'}", f"-I{work}", str(work / "run_gemm.cu"), f"-L{LIB_DIR}", "-lkpgemm",
                     f"-Xlinker", f"-rpath,{LIB_DIR}", "-o", str(work / "librun_gemm.so")],
                    check=True, capture_output=True, text=True)
-    assert (work / "librun_gemm.so").exists()
+    assert "run_gemm" in subprocess.run(["nm", "-D", str(work / "librun_gemm.so")], capture_output=True,
+                                        text=True).stdout
 
 
 def test_integration_doc_quotes_this_code():
