@@ -127,6 +127,13 @@ int kp_gemm_ex(int id, int m, int k, int n, int batch,
 int kp_set_max_k_slices(int max_slices);
 int kp_gemm_plan(int id, int m, int k, int n, int batch, int num_sms, int* k_slices, int* k_per_slice);
 
+/* SIMT-family operand staging (a launch detail; results are bit-identical either way):
+ * 1 = TMA bulk tensor copies + mbarriers wherever the operand rows are 16-byte
+ * aligned and the CTA tile is <= 256 columns wide (default), 0 = per-thread cp.async
+ * copies with one CTA barrier per k-tile everywhere.  Returns the previous mode; any
+ * other value is -EINVAL. */
+int kp_set_simt_staging(int mode);
+
 /* ---- benchmark harness ---------------------------------------------------
  * warmup untimed launches, then one launch timed alone to size the loop, then
  * max(min_iters, ceil(min_ms / t1)) (capped at max_iters) back-to-back launches

@@ -16,6 +16,8 @@
 #include "kpgemm.h"
 #include "tc_families.h"
 
+std::atomic<int> kp::g_f1_tma_staging{1};  // kp_set_simt_staging
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -386,6 +388,11 @@ int kp_set_max_k_slices(int max_slices) {
   if (max_slices < 1 || max_slices > kp::kMaxKSlices)
     return fail(KP_EINVAL, "max k-slices must be in [1, %d], got %d", kp::kMaxKSlices, max_slices);
   return g_max_kslices.exchange(max_slices);
+}
+
+int kp_set_simt_staging(int mode) {
+  if (mode != 0 && mode != 1) return fail(KP_EINVAL, "staging mode must be 0 (cp.async) or 1 (TMA), got %d", mode);
+  return kp::g_f1_tma_staging.exchange(mode);
 }
 
 int kp_gemm_plan(int id, int m, int k, int n, int batch, int num_sms, int* k_slices, int* k_per_slice) {

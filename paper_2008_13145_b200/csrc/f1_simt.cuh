@@ -25,11 +25,50 @@
 #pragma once
 
 #include <cooperative_groups.h>
+#include <cuda.h>
+
+#include <cstring>
 
 #include "common.cuh"
 #include "families.h"
 
 namespace kp {
+
+// ---- TMA staging (bulk tensor copies + mbarrier) -----------------------------
+// The operand tensor maps of one launch (unused by the cp.async path).
+struct F1Maps {
+  CUtensorMap a, b;
+};
+
+__device__ __forceinline__ uint32_t f1_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void f1_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(f1_smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void f1_mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(f1_smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void f1_mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "KP_F1_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra KP_F1_WAIT_%=;\n"
+      "}\n" ::"r"(f1_smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void f1_tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                               int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+          "r"(f1_smem_u32(dst)),
+      "l"(map), "r"(f1_smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
 
 constexpr int f1_pick_wtc(int R, int C, int WGR, int WGC) {
   int best = -1, best_cost = 1 << 30;
@@ -91,6 +130,21 @@ struct F1Cfg {
   // the row-fastest lane order costs more in the epilogue than it saves.
   static constexpr bool PAIR_B = VC == 4 && COST_PAIR_B < COST_PAIR_A;
   static constexpr bool B_CHUNKS = (BN % 4) == 0;
+  // TMA staging variant: the same smem layout (LHS rows padded to SA floats, RHS rows
+  // of BN floats) written by bulk tensor copies -- the LHS box is SA = BK + 4 floats
+  // wide, so the pad columns arrive as the next k-tile's first floats (never read) and
+  // the padded layout needs no swizzle.  Boxes are <= 256 rows; the RHS box is one
+  // BN-wide row block, so TMA staging needs BN <= 256 and BN % 4 == 0.
+  static constexpr int A_BOX_ROWS = BM < 256 ? BM : 256;
+  static constexpr int A_BOXES = (BM + A_BOX_ROWS - 1) / A_BOX_ROWS;
+  static constexpr int T_B_OFF = (BM * SA + 31) / 32 * 32;  // floats; 128-byte aligned RHS
+  static constexpr int T_STAGE = (T_B_OFF + BK * BN + 31) / 32 * 32;
+  static constexpr int T_TX_BYTES = 4 * (A_BOXES * A_BOX_ROWS * SA + BK * BN);
+  static constexpr bool TMA_OK = B_CHUNKS && BN <= 256;
+  // full barriers and arrival counters sit past both the ring and the sliced launches'
+  // partial tile (which reuses the ring); +128 bytes to align the dynamic base
+  static constexpr int T_BAR_OFF = ((STAGES * T_STAGE > BM * SP ? STAGES * T_STAGE : BM * SP) * 4 + 15) / 16 * 16;
+  static constexpr int T_SMEM_BYTES = T_BAR_OFF + STAGES * 12 + 128;
   static_assert(WTC > 0, "work group not tileable by warps");
   static_assert(NT % 32 == 0, "work group must be whole warps");
   static_assert(BK % A == 0, "stage depth must be a multiple of A");
@@ -154,12 +208,25 @@ __device__ __forceinline__ void f1_slice_reduce(const GemmArgs& p, float* smem, 
   cl.sync();  // keep this CTA's partial alive until every rank has read it
 }
 
-template <int R, int A, int C, int WGR, int WGC>
-__global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCKS) f1_kernel(GemmArgs p, int groups_n) {
+// TMA = false: every thread stages its share of each k-tile with cp.async and the CTA
+// syncs once per k-tile.  TMA = true (16-byte-aligned operand rows, BN <= 256): bulk
+// tensor copies fill the same layout; each stage has a full mbarrier (the copies'
+// transaction bytes) and an arrival counter -- every warp waits on the stage's barrier,
+// runs its outer products, and its lane 0 counts the stage as consumed; the warp that
+// completes the count refills the stage with the k-tile STAGES ahead.  No CTA-wide
+// barrier and no per-thread copy address math in the main loop.
+template <int R, int A, int C, int WGR, int WGC, bool TMA>
+__global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCKS)
+    f1_kernel(GemmArgs p, int groups_n, const __grid_constant__ F1Maps maps) {
   using Cfg = F1Cfg<R, A, C, WGR, WGC>;
   constexpr int NT = Cfg::NT, BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
   constexpr int SA = Cfg::SA, SB = Cfg::SB, STAGES = Cfg::STAGES, VC = Cfg::VC;
-  extern __shared__ __align__(16) float smem[];
+  extern __shared__ __align__(16) float smem_dyn[];
+  float* smem = smem_dyn;
+  if constexpr (TMA) {  // bulk tensor copies need 128-byte-aligned destinations
+    const uint32_t s0 = f1_smem_u32(smem_dyn);
+    smem = smem_dyn + (((s0 + 127u) & ~127u) - s0) / 4;
+  }
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -264,23 +331,9 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
   const int KTall = (k + BK - 1) / BK;
   const int kt0 = static_cast<int>(blockIdx.z) * p.kt_per_slice;
   const int KT = min(KTall - kt0, p.kt_per_slice);
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_tile(s, kt0 + s);
-    cp_async_commit();
-  }
 
-  for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      const int nk = kt + STAGES - 1;
-      if (nk < KT) load_tile(nk % STAGES, kt0 + nk);
-      cp_async_commit();
-    }
-    const float* as = smem + (kt % STAGES) * Cfg::STAGE;
-    const float* bs = as + BM * SA;
-    if (!warp_live) continue;  // this warp's whole block lies outside the problem
+  // The outer products of one staged k-tile (both staging paths share the layout).
+  auto tile_math = [&](const float* as, const float* bs) {
 #pragma unroll
     for (int kk = 0; kk < BK; kk += A) {
       float a[R][A];
@@ -303,8 +356,72 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
         }
       }
     }
+  };
+
+  if constexpr (TMA) {
+    constexpr int NW = NT / 32;
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + Cfg::T_BAR_OFF);
+    int* consumed = reinterpret_cast<int*>(full + STAGES);
+    const int za = (p.batch > 1 && p.sA != 0) ? b : 0;
+    const int zb = (p.batch > 1 && p.sB != 0) ? b : 0;
+    auto issue = [&](int stage, int kt) {  // one thread: the k-tile's boxes into a stage
+      float* as = smem + stage * Cfg::T_STAGE;
+      f1_mbar_expect_tx(&full[stage], Cfg::T_TX_BYTES);
+#pragma unroll
+      for (int i = 0; i < Cfg::A_BOXES; ++i)
+        f1_tma_load_3d(as + i * Cfg::A_BOX_ROWS * SA, &maps.a, &full[stage], kt * BK,
+                       static_cast<int>(m0) + i * Cfg::A_BOX_ROWS, za);
+      f1_tma_load_3d(as + Cfg::T_B_OFF, &maps.b, &full[stage], static_cast<int>(n0), kt * BK, zb);
+    };
+    if (tid == 0) {
+#pragma unroll
+      for (int s = 0; s < STAGES; ++s) {
+        f1_mbar_init(&full[s], 1);
+        consumed[s] = 0;
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int s = 0; s < STAGES && s < KT; ++s) issue(s, kt0 + s);
+    }
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % STAGES;
+      f1_mbar_wait(&full[s], (kt / STAGES) & 1);
+      const float* as = smem + s * Cfg::T_STAGE;
+      if (warp_live) tile_math(as, as + Cfg::T_B_OFF);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();  // this warp's reads of the stage happen before the count
+        const int prior = atomicAdd(&consumed[s], 1);
+        if ((prior + 1) % NW == 0 && kt + STAGES < KT) {  // last consumer refills the stage
+          __threadfence_block();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(s, kt0 + kt + STAGES);
+        }
+      }
+    }
+    __syncthreads();  // every stage consumed (no copy in flight) before smem is reused
+  } else {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < KT) load_tile(s, kt0 + s);
+      cp_async_commit();
+    }
+    for (int kt = 0; kt < KT; ++kt) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      {
+        const int nk = kt + STAGES - 1;
+        if (nk < KT) load_tile(nk % STAGES, kt0 + nk);
+        cp_async_commit();
+      }
+      const float* as = smem + (kt % STAGES) * Cfg::STAGE;
+      if (warp_live) tile_math(as, as + BM * SA);  // else: the warp's block lies outside the problem
+    }
+    cp_async_wait<0>();
   }
-  cp_async_wait<0>();
 
   if (p.kslices > 1) {
     // k-sliced: park the partial tile in this CTA's shared memory, then each CTA of
@@ -359,11 +476,13 @@ cudaError_t f1_set_attributes() {
   using Cfg = F1Cfg<R, A, C, WGR, WGC>;
   static bool attr_set = false;  // benign race: idempotent attribute writes
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(f1_kernel<R, A, C, WGR, WGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SLICE_SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(f1_kernel<R, A, C, WGR, WGC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
+    for (auto fn : {f1_kernel<R, A, C, WGR, WGC, false>, f1_kernel<R, A, C, WGR, WGC, true>}) {
+      const int bytes = fn == f1_kernel<R, A, C, WGR, WGC, true> ? Cfg::T_SMEM_BYTES : Cfg::SLICE_SMEM_BYTES;
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
     attr_set = true;
   }
   return cudaSuccess;
@@ -376,7 +495,6 @@ int f1_cluster_fit(int slices) {
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(1, 1, slices);
   lc.blockDim = dim3(Cfg::NT);
-  lc.dynamicSmemBytes = Cfg::SLICE_SMEM_BYTES;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 1;
@@ -384,12 +502,56 @@ int f1_cluster_fit(int slices) {
   at[0].val.clusterDim.z = slices;
   lc.attrs = at;
   lc.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, f1_kernel<R, A, C, WGR, WGC>, &lc) != cudaSuccess) {
-    cudaGetLastError();
-    return -1;
+  // the planner does not know the operands' alignment: report the smaller fit of the
+  // two staging paths
+  int best = -1;
+  for (int t = 0; t < 2; ++t) {
+    int n = 0;
+    lc.dynamicSmemBytes = t ? Cfg::T_SMEM_BYTES : Cfg::SLICE_SMEM_BYTES;
+    const cudaError_t e = t ? cudaOccupancyMaxActiveClusters(&n, f1_kernel<R, A, C, WGR, WGC, true>, &lc)
+                            : cudaOccupancyMaxActiveClusters(&n, f1_kernel<R, A, C, WGR, WGC, false>, &lc);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return -1;
+    }
+    best = best < 0 ? n : (n < best ? n : best);
   }
-  return n;
+  return best;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda symbol
+// needed at this call site).
+using F1EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline F1EncodeFn f1_encode_fn() {
+  static F1EncodeFn fn = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<F1EncodeFn>(ptr);
+    return static_cast<F1EncodeFn>(nullptr);
+  }();
+  return fn;
+}
+
+// A 3-d fp32 tensor map (inner dim0, rows dim1, batch dim2) with an unswizzled box.
+// A zero batch stride (broadcast operand) becomes a batch extent of 1.
+inline bool f1_encode(CUtensorMap* map, const void* base, int64_t d0, int64_t d1, int64_t ld, int64_t sbatch,
+                      int batch, int box0, int box1) {
+  F1EncodeFn enc = f1_encode_fn();
+  if (!enc) return false;
+  const bool batched = batch > 1 && sbatch != 0;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d0), static_cast<cuuint64_t>(d1),
+                        static_cast<cuuint64_t>(batched ? batch : 1)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 4,
+                           static_cast<cuuint64_t>(batched ? sbatch : (ld * d1 + 3) / 4 * 4) * 4};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(box0), static_cast<cuuint32_t>(box1), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int R, int A, int C, int WGR, int WGC>
@@ -401,6 +563,7 @@ cudaError_t f1_launch(const GemmArgs& p0, cudaStream_t s) {
   p.a_vec = (p.k % 4 == 0) && (p.lda % 4 == 0) && (p.sA % 4 == 0) && aligned(p.A, 16);
   p.b_vec = (p.n % 4 == 0) && (p.ldb % 4 == 0) && (p.sB % 4 == 0) && aligned(p.B, 16);
   p.c_vec = (p.ldc % Cfg::VC == 0) && (p.sC % Cfg::VC == 0) && aligned(p.C, 4 * Cfg::VC);
+  p.c_vec4 = (p.ldc % 4 == 0) && (p.sC % 4 == 0) && aligned(p.C, 16);
   const int64_t groups_m = (p.m + Cfg::BM - 1) / Cfg::BM;
   const int64_t groups_n = (p.n + Cfg::BN - 1) / Cfg::BN;
   const int64_t gx = groups_m * groups_n;
@@ -408,16 +571,48 @@ cudaError_t f1_launch(const GemmArgs& p0, cudaStream_t s) {
   if (p.kslices <= 1) {
     p.kslices = 1;
     p.kt_per_slice = (p.k + Cfg::BK - 1) / Cfg::BK;
-    f1_kernel<R, A, C, WGR, WGC><<<dim3(static_cast<unsigned>(gx), p.batch), Cfg::NT, Cfg::SMEM_BYTES, s>>>(
-        p, static_cast<int>(groups_n));
-    return cudaGetLastError();
+  } else if (p.kslices > kMaxKSlices) {
+    return cudaErrorInvalidConfiguration;
   }
-  if (p.kslices > kMaxKSlices) return cudaErrorInvalidConfiguration;
-  p.c_vec4 = (p.ldc % 4 == 0) && (p.sC % 4 == 0) && aligned(p.C, 16);
+  // TMA staging: rows 16-byte aligned in both operands (the tensor maps' stride rule;
+  // k and n themselves may be ragged -- the boxes zero-fill past them), coordinates
+  // within int range.
+  const bool tma = Cfg::TMA_OK && g_f1_tma_staging.load(std::memory_order_relaxed) != 0 && aligned(p.A, 16) && aligned(p.B, 16) && p.lda % 4 == 0 &&
+                   p.ldb % 4 == 0 && (p.batch == 1 || ((p.sA % 4 == 0) && (p.sB % 4 == 0))) &&
+                   p.m < (1LL << 31) - Cfg::BM && p.k < (1 << 30);
+  F1Maps maps;
+  if (tma) {
+    // one-entry cache per instantiation and host thread: sweeps and layer loops re-launch
+    // the same operands, and encoding costs ~1 us of host time
+    struct Key {
+      const void *pa, *pb;
+      int64_t m, k, n, batch, lda, ldb, sA, sB;
+      bool operator==(const Key& o) const { return std::memcmp(this, &o, sizeof(Key)) == 0; }
+    };
+    thread_local Key last_key;
+    thread_local F1Maps last_maps;
+    thread_local bool have = false;
+    Key key;
+    std::memset(&key, 0, sizeof(key));
+    key.pa = p.A; key.pb = p.B; key.m = p.m; key.k = p.k; key.n = p.n; key.batch = p.batch;
+    key.lda = p.lda; key.ldb = p.ldb; key.sA = p.sA; key.sB = p.sB;
+    if (!(have && key == last_key)) {
+      if (!f1_encode(&last_maps.a, p.A, p.k, p.m, p.lda, p.sA, p.batch, Cfg::SA, Cfg::A_BOX_ROWS) ||
+          !f1_encode(&last_maps.b, p.B, p.n, p.k, p.ldb, p.sB, p.batch, Cfg::BN, Cfg::BK)) {
+        have = false;
+        return cudaErrorInvalidValue;
+      }
+      last_key = key;
+      have = true;
+    }
+    maps = last_maps;
+  } else {
+    std::memset(&maps, 0, sizeof(maps));
+  }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(static_cast<unsigned>(gx), p.batch, p.kslices);
   lc.blockDim = dim3(Cfg::NT);
-  lc.dynamicSmemBytes = Cfg::SLICE_SMEM_BYTES;
+  lc.dynamicSmemBytes = tma ? Cfg::T_SMEM_BYTES : (p.kslices > 1 ? Cfg::SLICE_SMEM_BYTES : Cfg::SMEM_BYTES);
   lc.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -425,8 +620,10 @@ cudaError_t f1_launch(const GemmArgs& p0, cudaStream_t s) {
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = p.kslices;
   lc.attrs = at;
-  lc.numAttrs = 1;
-  return cudaLaunchKernelEx(&lc, f1_kernel<R, A, C, WGR, WGC>, p, static_cast<int>(groups_n));
+  lc.numAttrs = p.kslices > 1 ? 1 : 0;
+  const int gn = static_cast<int>(groups_n);
+  return tma ? cudaLaunchKernelEx(&lc, f1_kernel<R, A, C, WGR, WGC, true>, p, gn, maps)
+             : cudaLaunchKernelEx(&lc, f1_kernel<R, A, C, WGR, WGC, false>, p, gn, maps);
 }
 
 }  // namespace kp

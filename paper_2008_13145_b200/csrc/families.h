@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace kp {
@@ -26,6 +28,9 @@ struct F1Entry {
   // cudaOccupancyMaxActiveClusters for a (1, 1, slices) cluster launch (< 0: error)
   int (*cluster_fit)(int slices);
 };
+// SIMT operand staging mode (kp_set_simt_staging): 1 = TMA where eligible, 0 = cp.async.
+extern std::atomic<int> g_f1_tma_staging;
+
 constexpr int kMaxKSlices = 16;      // non-portable thread-block-cluster limit on sm_100
 constexpr int kDefaultKSlices = 8;   // portable clusters: measured faster than 9..16
 

@@ -223,6 +223,17 @@ def set_max_k_slices(max_slices: int) -> int:
     return _lib.check(_lib.load().kp_set_max_k_slices(int(max_slices)), "kp_set_max_k_slices")
 
 
+def set_simt_staging(mode: str) -> str:
+    """SIMT operand staging: "tma" (bulk tensor copies + mbarriers wherever the rows are
+    16-byte aligned; the default) or "cp.async" (per-thread copies).  Results are
+    bit-identical; returns the previous mode."""
+    modes = {"cp.async": 0, "tma": 1}
+    if mode not in modes:
+        raise ValueError(f"staging mode must be one of {sorted(modes)}, got {mode!r}")
+    prev = _lib.check(_lib.load().kp_set_simt_staging(modes[mode]), "kp_set_simt_staging")
+    return "tma" if prev else "cp.async"
+
+
 def ffma_peak_tflops(packed: bool = False, stream: torch.cuda.Stream | None = None) -> float:
     """Measured FP32 peak of the current device (kp_ffma_peak): scalar FFMA or,
     with ``packed``, sm_100 FFMA2."""

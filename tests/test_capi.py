@@ -154,3 +154,18 @@ def test_k_slice_plan_host_logic(lib):
     finally:
         assert gemm.set_max_k_slices(prev) == 1
     assert lib.kp_set_max_k_slices(0) == _lib.KP_EINVAL
+
+
+def test_simt_staging_switch(lib):
+    from paper_2008_13145_b200 import gemm
+
+    """kp_set_simt_staging: 1 (TMA, default) / 0 (cp.async), previous mode returned."""
+    assert gemm.set_simt_staging("cp.async") == "tma"
+    try:
+        assert gemm.set_simt_staging("cp.async") == "cp.async"
+    finally:
+        assert gemm.set_simt_staging("tma") == "cp.async"
+    assert lib.kp_set_simt_staging(2) == _lib.KP_EINVAL
+    assert lib.kp_set_simt_staging(-1) == _lib.KP_EINVAL
+    with pytest.raises(ValueError):
+        gemm.set_simt_staging("ldgsts")

@@ -69,6 +69,46 @@ def test_all_640_configs_single_chain_when_unsliced(cuda_device, shape):
     assert not bad, f"{len(bad)} configs differ, e.g. {bad[:5]}"
 
 
+@pytest.mark.parametrize("shape,pad_k,pad_n", [((37, 27, 61, 3), 1, 3), ((33, 147, 70, 2), 1, 2),
+                                               ((300, 50, 130, 1), 2, 2)])
+def test_all_640_configs_bit_exact_tma_ragged(cuda_device, shape, pad_k, pad_n):
+    """Ragged k and n inside 16-byte-aligned rows (lda, ldb multiples of 4): the SIMT
+    family stages these with TMA boxes whose k/n tails are zero-filled by the copy
+    engine -- still bit-exact against the oracle for every config."""
+    A, B = _pair(*shape)
+    bigA = np.pad(A, ((0, 0), (0, 0), (0, pad_k)))
+    bigB = np.pad(B, ((0, 0), (0, 0), (0, pad_n)))
+    assert bigA.shape[2] % 4 == 0 and bigB.shape[2] % 4 == 0
+    m, k, n, _ = shape
+    dA = torch.from_numpy(bigA).to(cuda_device)[:, :, :k]
+    dB = torch.from_numpy(bigB).to(cuda_device)[:, :, :n]
+    cache, bad = {}, []
+    for cfg in CONFIGS:
+        got = gemm.matmul(dA, dB, cfg, "simt").cpu().numpy()
+        if not np.array_equal(_bits(got), _want(A, B, cfg, "simt", cache)):
+            bad.append(cfg.as_tuple())
+    assert not bad, f"{len(bad)} configs differ, e.g. {bad[:5]}"
+
+
+@pytest.mark.parametrize("shape", [(64, 128, 96, 1), (200, 96, 64, 2), (96, 1000, 256, 1)])
+def test_simt_staging_paths_bit_identical(cuda_device, shape):
+    """TMA and cp.async staging of the same launch produce the same bits (and the oracle's)."""
+    A, B = _pair(*shape)
+    dA, dB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    cache, bad = {}, []
+    prev = gemm.set_simt_staging("cp.async")
+    try:
+        ref = {c: gemm.matmul(dA, dB, c, "simt").cpu().numpy() for c in CONFIGS}
+    finally:
+        gemm.set_simt_staging(prev)
+    for cfg in CONFIGS:
+        got = gemm.matmul(dA, dB, cfg, "simt").cpu().numpy()
+        if not (np.array_equal(_bits(got), _bits(ref[cfg])) and
+                np.array_equal(_bits(got), _want(A, B, cfg, "simt", cache))):
+            bad.append(cfg.as_tuple())
+    assert not bad, f"{len(bad)} configs differ, e.g. {bad[:5]}"
+
+
 EDGE = [1, 7, 31, 64, 255, 256, 1000]
 
 
