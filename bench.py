@@ -356,7 +356,7 @@ def e2e_layers(args, world, device, stream, disp, bufs, step_flops, in_dtype):
     only (im2col is extra work inside the timed region)."""
     import torch
 
-    from paper_2008_13145_b200 import _lib, shapes
+    from paper_2008_13145_b200 import _lib, gemm, shapes
 
     lib = _lib.load()
     geo = {}
@@ -366,7 +366,7 @@ def e2e_layers(args, world, device, stream, disp, bufs, step_flops, in_dtype):
     for layer in shapes.VGG16_LAYERS:
         names += [layer.name] * layer.count
     gen = torch.Generator().manual_seed(99)
-    host_in, dev_in, scratch = [], [], {}
+    host_in, dev_in = [], []
     for (name, p, A, W, C, vid), lname in zip(bufs, names):
         g = geo[lname]
         shape = (args.batch, g[0], g[0], g[1]) if g else (p.m, p.k)
@@ -377,32 +377,33 @@ def e2e_layers(args, world, device, stream, disp, bufs, step_flops, in_dtype):
     h2d = sum(t.numel() * t.element_size() for t in host_in)
     d2h = sum(t.numel() * t.element_size() for t in host_out)
     bf16 = in_dtype == torch.bfloat16
-    if bf16:
-        biggest = max(p.m * p.k for _, p, *_ in bufs)
-        scratch = torch.empty(biggest, device=device)
     h2d_stream, d2h_stream = torch.cuda.Stream(device), torch.cuda.Stream(device)
     landed = [torch.cuda.Event() for _ in bufs]
     computed = [torch.cuda.Event() for _ in bufs]
     s_handle = stream.cuda_stream
     launches = [0]
 
+    implicit = [geo[lname] is not None and not bf16 and gemm.conv3x3_supported(vid, geo[lname][1], p.n)
+                for (name, p, A, W, C, vid), lname in zip(bufs, names)]
+
     def lower(i, lname, p, A):
-        """Device-side operand for layer i: im2col (conv) / cast (bf16) into A."""
+        """Device-side operand for layer i: im2col (conv, into A's pitched rows) / cast
+        (bf16 fc) into A."""
         g = geo[lname]
         x = dev_in[i]
         if g is None and not bf16:
             return x
-        target = scratch if bf16 else A
         if g is not None:
-            _lib.check(lib.kp_im2col3x3_nhwc(x.data_ptr(), args.batch, g[0], g[0], g[1], target.data_ptr(), p.k,
-                                             s_handle), "kp_im2col3x3_nhwc")
+            if bf16:
+                _lib.check(lib.kp_im2col3x3_nhwc_bf16(x.data_ptr(), args.batch, g[0], g[0], g[1], A.data_ptr(),
+                                                      A.stride(0), s_handle), "kp_im2col3x3_nhwc_bf16")
+            else:
+                _lib.check(lib.kp_im2col3x3_nhwc(x.data_ptr(), args.batch, g[0], g[0], g[1], A.data_ptr(),
+                                                 A.stride(0), s_handle), "kp_im2col3x3_nhwc")
             launches[0] += 1
-            src = target
-        else:
-            src = x
-        if bf16:
-            _lib.check(lib.kp_cast_bf16(src.data_ptr(), p.m * p.k, A.data_ptr(), s_handle), "kp_cast_bf16")
-            launches[0] += 1
+            return A
+        _lib.check(lib.kp_cast_bf16(x.data_ptr(), p.m * p.k, A.data_ptr(), s_handle), "kp_cast_bf16")
+        launches[0] += 1
         return A
 
     def e2e_step():
@@ -412,8 +413,16 @@ def e2e_layers(args, world, device, stream, disp, bufs, step_flops, in_dtype):
                 landed[i].record(h2d_stream)
         for i, ((name, p, A, W, C, vid), lname) in enumerate(zip(bufs, names)):
             stream.wait_event(landed[i])
-            operand = lower(i, lname, p, A)
-            disp.matmul(operand.view(p.m, p.k), W, out=C, stream=stream)
+            g = geo[lname]
+            if g is not None and implicit[i]:
+                # implicit GEMM: the dispatched variant gathers the patches from the NHWC
+                # activation with TMA im2col copies (kp_conv3x3_nhwc_ex), no im2col pass
+                x = dev_in[i]
+                _lib.check(lib.kp_conv3x3_nhwc_ex(vid, x.data_ptr(), args.batch, g[0], g[0], g[1], W.data_ptr(), p.n,
+                                                  C.data_ptr(), None, 0, s_handle), "kp_conv3x3_nhwc_ex")
+            else:
+                operand = lower(i, lname, p, A)
+                disp.matmul(operand, W, out=C, stream=stream)
             launches[0] += 1
             computed[i].record(stream)
             d2h_stream.wait_event(computed[i])
@@ -440,8 +449,10 @@ def e2e_layers(args, world, device, stream, disp, bufs, step_flops, in_dtype):
     return {"value": step_flops * args.steps * world / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
             "launches_per_step": launches[0] // args.steps,
-            "path": "host NHWC activations -> H2D -> kp_im2col3x3_nhwc" + (" + kp_cast_bf16" if bf16 else "")
-                    + " -> Dispatcher.matmul (kp_gemm) -> D2H of every layer output"}
+            "implicit_conv_layers": sum(implicit),
+            "path": "host NHWC activations -> H2D -> conv layers: kp_conv3x3_nhwc_ex (implicit GEMM, TMA im2col) "
+                    "where the dispatched variant supports it, else kp_im2col3x3_nhwc" +
+                    (" + kp_cast_bf16" if bf16 else "") + " + Dispatcher.matmul (kp_gemm) -> D2H of every layer output"}
 
 
 # ---------------------------------------------------------------------- ours --
@@ -460,8 +471,9 @@ def run_ours(args, world, rank, local):
     in_dtype = gemm.input_dtype(args.family)  # fp32, or bf16 operands for the BF16 family
     gen = torch.Generator(device=device).manual_seed(1234 + rank)
     bufs = []
+    al = 16 // in_dtype.itemsize  # rows pitched to 16 bytes, as the sweep times them (conv1_1: k = 27)
     for name, p in layers:
-        A = (torch.rand(p.m, p.k, device=device, generator=gen) * 2 - 1).to(in_dtype)
+        A = (torch.rand(p.m, -(-p.k // al) * al, device=device, generator=gen) * 2 - 1).to(in_dtype)[:, :p.k]
         W = ((torch.rand(p.k, p.n, device=device, generator=gen) * 2 - 1) * math.sqrt(6.0 / p.k)).to(in_dtype)
         C = torch.empty(p.m, p.n, device=device)
         bufs.append((name, p, A, W, C, disp.variant(p)))

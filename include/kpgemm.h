@@ -208,6 +208,17 @@ int kp_im2col3x3_nhwc_pad(const float* x, int B, int H, int W, int C, float* out
  * cast of n elements (n % 8 == 0, 16-byte-aligned pointers). */
 int kp_im2col3x3_nhwc_bf16(const float* x, int B, int H, int W, int C, void* out, int kpad, void* stream);
 int kp_cast_bf16(const float* x, int64_t n, void* out, void* stream);
+/* Implicit-GEMM 3x3 / stride 1 / pad 1 convolution (SIMT family): the GEMM that
+ * kp_im2col3x3_nhwc + kp_gemm_ex would run (m = B*H*W, k = 9*C, n = Cout, weights
+ * (9*C) x Cout row-major, out (B*H*W) x Cout = NHWC) with the patch rows gathered
+ * straight from x by TMA im2col copies -- no im2col buffer in HBM.  Same launch plan
+ * (k-slices) and fp32 chain as the explicit path, so the output is bit-identical.
+ * kp_conv3x3_supported(id, C, Cout) returns 1 when variant id can run it (SIMT variant
+ * with TMA staging, i.e. CTA tile <= 256 columns, C a multiple of its k-tile depth,
+ * Cout % 4 == 0), 0 when not, < 0 for a bad id.  x, w and out must be 16-byte aligned. */
+int kp_conv3x3_supported(int id, int C, int Cout);
+int kp_conv3x3_nhwc_ex(int id, const float* x, int B, int H, int W, int C, const float* w, int Cout, float* out,
+                       const float* bias, int flags, void* stream);
 /* 2x2 / stride 2 max pooling, NHWC: (B, H, W, C) -> (B, H/2, W/2, C). */
 int kp_maxpool2x2_nhwc(const float* x, int B, int H, int W, int C, float* out, void* stream);
 

@@ -291,6 +291,7 @@ kp::GemmArgs make_args(int m, int k, int n, int batch, const void* A, int64_t ld
   p.kslices = 1;
   p.kt_per_slice = 0;
   p.tail_tiles = p.tail_slices = 0;
+  p.conv_h = p.conv_w = p.conv_c = 0;
   p.bias = nullptr;
   p.relu = 0;
   return p;
@@ -379,6 +380,37 @@ int kp_gemm_ex(int id, int m, int k, int n, int batch, const void* A, int64_t ld
   if (rc != KP_OK) return rc;
   if (flags & ~KP_EPI_RELU) return fail(KP_EINVAL, "unknown epilogue flags 0x%x", flags);
   kp::GemmArgs p = make_args(m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC);
+  p.bias = bias;
+  p.relu = (flags & KP_EPI_RELU) != 0;
+  return launch(id, p, static_cast<cudaStream_t>(stream));
+}
+
+int kp_conv3x3_supported(int id, int C, int Cout) {
+  Registry& reg = registry();
+  if (id < 0 || id >= static_cast<int>(reg.variants.size())) return fail(KP_ENOENT, "unknown variant id %d", id);
+  const Variant& v = reg.variants[id];
+  if (v.family != KP_FAMILY_SIMT || C < 1 || Cout < 1) return 0;
+  const kp::F1Entry& e = reg.f1[v.index];
+  return (e.tma_ok && C % e.bk == 0 && Cout % 4 == 0) ? 1 : 0;
+}
+
+int kp_conv3x3_nhwc_ex(int id, const float* x, int B, int H, int W, int C, const float* w, int Cout, float* out,
+                       const float* bias, int flags, void* stream) {
+  if (B < 1 || H < 1 || W < 1 || C < 1 || Cout < 1) return fail(KP_EINVAL, "conv dims must be >= 1");
+  if (static_cast<int64_t>(B) * H * W > 0x7fffffffLL || 9LL * C > 0x7fffffffLL)
+    return fail(KP_EINVAL, "conv too large for 32-bit GEMM dims");
+  const int rc = kp_conv3x3_supported(id, C, Cout);
+  if (rc < 0) return rc;
+  if (rc == 0) return fail(KP_EINVAL, "variant %d cannot run an implicit conv with C = %d, Cout = %d", id, C, Cout);
+  if (!x || !w || !out) return fail(KP_EINVAL, "null operand pointer");
+  auto aligned = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) % 16) == 0; };
+  if (!aligned(x) || !aligned(w) || !aligned(out)) return fail(KP_EINVAL, "x, w and out must be 16-byte aligned");
+  if (flags & ~KP_EPI_RELU) return fail(KP_EINVAL, "unknown epilogue flags 0x%x", flags);
+  const int m = B * H * W, k = 9 * C;
+  kp::GemmArgs p = make_args(m, k, Cout, 1, x, k, 0, w, Cout, 0, out, Cout, 0);
+  p.conv_h = H;
+  p.conv_w = W;
+  p.conv_c = C;
   p.bias = bias;
   p.relu = (flags & KP_EPI_RELU) != 0;
   return launch(id, p, static_cast<cudaStream_t>(stream));

@@ -37,6 +37,11 @@ struct GemmArgs {
   // the persistent kernel) run as a second, k-sliced launch with tail_slices slices.
   int tail_tiles;
   int tail_slices;
+  // Implicit-GEMM 3x3 / stride 1 / pad 1 convolution (SIMT TMA staging only): when
+  // conv_c > 0, A is the NHWC activation (batch = m / (conv_h * conv_w) images of
+  // conv_h x conv_w x conv_c) and row r / column k of the GEMM operand is the im2col
+  // patch value kp_im2col3x3_nhwc would write, gathered by TMA im2col copies.
+  int conv_h, conv_w, conv_c;
 };
 
 // Epilogue of every family: bias add (fp32, round-to-nearest) then ReLU.  Applied

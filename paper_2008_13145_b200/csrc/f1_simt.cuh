@@ -70,6 +70,18 @@ __device__ __forceinline__ void f1_tma_load_3d(void* dst, const CUtensorMap* map
       : "memory");
 }
 
+// TMA im2col copy: pixelsPerColumn consecutive output pixels (w fastest, then h, then
+// image) starting at base pixel (w, h, n) of the map's bounding box, each contributing
+// channelsPerPixel channels from c of input pixel (w + dx, h + dy); zero outside.
+__device__ __forceinline__ void f1_tma_im2col_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c, int w,
+                                                 int h, int n, uint16_t dx, uint16_t dy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2], {%7, %8};" ::"r"(f1_smem_u32(dst)),
+      "l"(map), "r"(f1_smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(dx), "h"(dy)
+      : "memory");
+}
+
 constexpr int f1_pick_wtc(int R, int C, int WGR, int WGC) {
   int best = -1, best_cost = 1 << 30;
   for (int wtc = 1; wtc <= 32; wtc *= 2) {
@@ -367,10 +379,23 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
     auto issue = [&](int stage, int kt) {  // one thread: the k-tile's boxes into a stage
       float* as = smem + stage * Cfg::T_STAGE;
       f1_mbar_expect_tx(&full[stage], Cfg::T_TX_BYTES);
+      if (p.conv_c > 0) {
+        // implicit conv: k-tile kt lies inside one filter tap (conv_c % BK == 0)
+        const int k0 = kt * BK, tap = k0 / p.conv_c, c0 = k0 - tap * p.conv_c;
+        const uint16_t dy = static_cast<uint16_t>(tap / 3), dx = static_cast<uint16_t>(tap - 3 * (tap / 3));
 #pragma unroll
-      for (int i = 0; i < Cfg::A_BOXES; ++i)
-        f1_tma_load_3d(as + i * Cfg::A_BOX_ROWS * SA, &maps.a, &full[stage], kt * BK,
-                       static_cast<int>(m0) + i * Cfg::A_BOX_ROWS, za);
+        for (int i = 0; i < Cfg::A_BOXES; ++i) {
+          const int r = static_cast<int>(m0) + i * Cfg::A_BOX_ROWS;
+          const int t = r / p.conv_w, w = r - t * p.conv_w;
+          const int img = t / p.conv_h, h = t - img * p.conv_h;
+          f1_tma_im2col_4d(as + i * Cfg::A_BOX_ROWS * SA, &maps.a, &full[stage], c0, w - 1, h - 1, img, dx, dy);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < Cfg::A_BOXES; ++i)
+          f1_tma_load_3d(as + i * Cfg::A_BOX_ROWS * SA, &maps.a, &full[stage], kt * BK,
+                         static_cast<int>(m0) + i * Cfg::A_BOX_ROWS, za);
+      }
       f1_tma_load_3d(as + Cfg::T_B_OFF, &maps.b, &full[stage], static_cast<int>(n0), kt * BK, zb);
     };
     if (tid == 0) {
@@ -554,6 +579,36 @@ inline bool f1_encode(CUtensorMap* map, const void* base, int64_t d0, int64_t d1
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The im2col map of a 3x3 / stride 1 / pad 1 convolution over an NHWC activation of
+// `imgs` images: bounding box corners -1 / -1 (base pixel = output pixel - 1 in w and h),
+// tap offsets (dx, dy) in 0..2 passed per copy.
+using F1EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline bool f1_encode_im2col(CUtensorMap* map, const void* x, int imgs, int H, int W, int Cin, int channels,
+                             int pixels) {
+  static F1EncodeIm2colFn enc = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<F1EncodeIm2colFn>(ptr);
+    return static_cast<F1EncodeIm2colFn>(nullptr);
+  }();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(Cin), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                        static_cast<cuuint64_t>(imgs)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(Cin) * 4, static_cast<cuuint64_t>(W) * Cin * 4,
+                           static_cast<cuuint64_t>(H) * W * Cin * 4};
+  const int lower[2] = {-1, -1}, upper[2] = {-1, -1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(x), dims, strides, lower, upper,
+             static_cast<cuuint32_t>(channels), static_cast<cuuint32_t>(pixels), es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int R, int A, int C, int WGR, int WGC>
 cudaError_t f1_launch(const GemmArgs& p0, cudaStream_t s) {
   using Cfg = F1Cfg<R, A, C, WGR, WGC>;
@@ -577,16 +632,20 @@ cudaError_t f1_launch(const GemmArgs& p0, cudaStream_t s) {
   // TMA staging: rows 16-byte aligned in both operands (the tensor maps' stride rule;
   // k and n themselves may be ragged -- the boxes zero-fill past them), coordinates
   // within int range.
-  const bool tma = Cfg::TMA_OK && g_f1_tma_staging.load(std::memory_order_relaxed) != 0 && aligned(p.A, 16) && aligned(p.B, 16) && p.lda % 4 == 0 &&
+  const bool conv = p.conv_c > 0;
+  if (conv && !(Cfg::TMA_OK && p.conv_c % Cfg::BK == 0 && p.k == 9 * p.conv_c && p.batch == 1 &&
+                p.m % (p.conv_h * p.conv_w) == 0 && aligned(p.A, 16) && aligned(p.B, 16) && p.ldb % 4 == 0))
+    return cudaErrorInvalidValue;
+  const bool tma = conv || (Cfg::TMA_OK && g_f1_tma_staging.load(std::memory_order_relaxed) != 0 && aligned(p.A, 16) && aligned(p.B, 16) && p.lda % 4 == 0 &&
                    p.ldb % 4 == 0 && (p.batch == 1 || ((p.sA % 4 == 0) && (p.sB % 4 == 0))) &&
-                   p.m < (1LL << 31) - Cfg::BM && p.k < (1 << 30);
+                   p.m < (1LL << 31) - Cfg::BM && p.k < (1 << 30));
   F1Maps maps;
   if (tma) {
     // one-entry cache per instantiation and host thread: sweeps and layer loops re-launch
     // the same operands, and encoding costs ~1 us of host time
     struct Key {
       const void *pa, *pb;
-      int64_t m, k, n, batch, lda, ldb, sA, sB;
+      int64_t m, k, n, batch, lda, ldb, sA, sB, ch, cw, cc;
       bool operator==(const Key& o) const { return std::memcmp(this, &o, sizeof(Key)) == 0; }
     };
     thread_local Key last_key;
@@ -596,8 +655,13 @@ cudaError_t f1_launch(const GemmArgs& p0, cudaStream_t s) {
     std::memset(&key, 0, sizeof(key));
     key.pa = p.A; key.pb = p.B; key.m = p.m; key.k = p.k; key.n = p.n; key.batch = p.batch;
     key.lda = p.lda; key.ldb = p.ldb; key.sA = p.sA; key.sB = p.sB;
+    key.ch = p.conv_h; key.cw = p.conv_w; key.cc = p.conv_c;
     if (!(have && key == last_key)) {
-      if (!f1_encode(&last_maps.a, p.A, p.k, p.m, p.lda, p.sA, p.batch, Cfg::SA, Cfg::A_BOX_ROWS) ||
+      const bool a_ok =
+          conv ? f1_encode_im2col(&last_maps.a, p.A, p.m / (p.conv_h * p.conv_w), p.conv_h, p.conv_w, p.conv_c,
+                                  Cfg::SA, Cfg::A_BOX_ROWS)
+               : f1_encode(&last_maps.a, p.A, p.k, p.m, p.lda, p.sA, p.batch, Cfg::SA, Cfg::A_BOX_ROWS);
+      if (!a_ok ||
           !f1_encode(&last_maps.b, p.B, p.n, p.k, p.ldb, p.sB, p.batch, Cfg::BN, Cfg::BK)) {
         have = false;
         return cudaErrorInvalidValue;

@@ -22,7 +22,7 @@ void put(F1Entry* table) {
   constexpr int R = 1 << RI, A = 1 << AI, C = 1 << CI;
   using Cfg = F1Cfg<R, A, C, WGR, WGC>;
   const int cfg = ((RI * 4 + AI) * 4 + CI) * kNumWgPairs + KP_WG_INDEX;
-  table[cfg] = F1Entry{&f1_launch<R, A, C, WGR, WGC>, Cfg::BM, Cfg::BN, Cfg::BK, Cfg::MIN_BLOCKS,
+  table[cfg] = F1Entry{&f1_launch<R, A, C, WGR, WGC>, Cfg::BM, Cfg::BN, Cfg::BK, Cfg::MIN_BLOCKS, Cfg::TMA_OK ? 1 : 0,
                        &f1_cluster_fit<R, A, C, WGR, WGC>};
 }
 

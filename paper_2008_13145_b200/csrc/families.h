@@ -25,6 +25,7 @@ using GemmLaunchFn = cudaError_t (*)(const GemmArgs&, cudaStream_t);
 struct F1Entry {
   GemmLaunchFn launch;
   int bm, bn, bk, occ;
+  int tma_ok;  // TMA staging applies (16-byte-aligned rows assumed): CTA tile <= 256 columns
   // cudaOccupancyMaxActiveClusters for a (1, 1, slices) cluster launch (< 0: error)
   int (*cluster_fit)(int slices);
 };

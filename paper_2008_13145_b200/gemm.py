@@ -172,6 +172,39 @@ def matmul(A: torch.Tensor, B: torch.Tensor, config: KernelConfig, family: str =
     return _squeeze_like(ops.C, A, B)
 
 
+def conv3x3_supported(vid: int, cin: int, cout: int) -> bool:
+    """Whether variant ``vid`` runs an implicit-GEMM 3x3 conv (kp_conv3x3_supported)."""
+    return _lib.check(_lib.load().kp_conv3x3_supported(vid, cin, cout), "kp_conv3x3_supported") == 1
+
+
+def conv3x3(x: torch.Tensor, w: torch.Tensor, vid: int, bias: torch.Tensor | None = None, relu: bool = False,
+            out: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """3x3 / stride 1 / pad 1 convolution of NHWC ``x`` (B, H, W, Cin) fp32 with the
+    (9*Cin, Cout) weight matrix ``w`` (k order (dy, dx, c), as kp_im2col3x3_nhwc) as an
+    implicit GEMM on SIMT variant ``vid`` (TMA im2col copies; kp_conv3x3_nhwc_ex).  The
+    result, (B, H, W, Cout), is bit-identical to im2col + matmul with the same variant."""
+    if x.dim() != 4 or not x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous():
+        raise ValueError("x must be a contiguous (B, H, W, C) fp32 CUDA tensor")
+    B, H, W, C = x.shape
+    if w.shape[0] != 9 * C or w.dim() != 2 or w.dtype != torch.float32 or not w.is_contiguous() \
+            or w.device != x.device:
+        raise ValueError(f"w must be a contiguous ({9 * C}, Cout) fp32 tensor on {x.device}")
+    cout = w.shape[1]
+    if out is None:
+        out = torch.empty(B, H, W, cout, device=x.device)
+    elif (out.shape != (B, H, W, cout) or out.dtype != torch.float32 or not out.is_contiguous()
+          or out.device != x.device):
+        raise ValueError(f"out must be a contiguous ({B}, {H}, {W}, {cout}) fp32 tensor on {x.device}")
+    if bias is not None and (bias.shape != (cout,) or bias.dtype != torch.float32 or bias.device != x.device):
+        raise ValueError(f"bias must be a ({cout},) fp32 tensor on {x.device}")
+    s = (stream or torch.cuda.current_stream(x.device)).cuda_stream
+    _lib.check(_lib.load().kp_conv3x3_nhwc_ex(vid, x.data_ptr(), B, H, W, C, w.data_ptr(), cout, out.data_ptr(),
+                                              bias.data_ptr() if bias is not None else None,
+                                              _lib.KP_EPI_RELU if relu else 0, s),
+               f"kp_conv3x3_nhwc_ex(variant {vid}, {tuple(x.shape)} x {cout})")
+    return out
+
+
 def bench(vid: int, ops: GemmOperands, warmup: int = 1, min_iters: int = 2, max_iters: int = 10000,
           min_ms: float = 2.0, stream: torch.cuda.Stream | None = None) -> tuple[float, int]:
     """Mean milliseconds per launch by CUDA events (``kp_bench``) and the loop count."""

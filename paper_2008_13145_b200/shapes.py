@@ -91,6 +91,16 @@ def _unique(problems) -> list[ProblemSize]:
     return out
 
 
+# The paper's three sample problems (its Figure "sample"):
+# square-ish m=512 k=784 n=512 batch 16, rectangular m=512 k=4608 n=784, and the long
+# accumulation m=32 k=12321 n=27 -- swept beside the VGG16 rows.
+PAPER_SAMPLES: tuple[ProblemSize, ...] = (
+    ProblemSize(512, 784, 512, 16),
+    ProblemSize(512, 4608, 784, 1),
+    ProblemSize(32, 12321, 27, 1),
+)
+
+
 def network_problems(network: str, batches=DEFAULT_BATCHES) -> list[ProblemSize]:
     """Unique GEMM problems of a network over a batch list, batch-major order."""
     layers = NETWORKS[network]

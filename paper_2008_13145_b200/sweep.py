@@ -82,8 +82,8 @@ class CudaEventTimer:
     sized for the largest problem (U(-1, 1), seed 0) holds every copy.
     """
 
-    def __init__(self, family: str, problems, warmup: int = 2, min_ms: float = 5.0,
-                 max_iters: int = 2000, device: int = 0, seed: int = 0, repeats: int = 3):
+    def __init__(self, family: str, problems, warmup: int = 2, min_ms: float = 60.0,
+                 max_iters: int = 100000, device: int = 0, seed: int = 0, repeats: int = 3):
         import torch  # imported lazily: CPU-only callers never need it
 
         from . import gemm
@@ -98,9 +98,10 @@ class CudaEventTimer:
         dtype = gemm.input_dtype(family)
         # every buffer holds at least 2 x L2 of copies (operand rotation), plus alignment slack
         floor = (2 * self.l2_bytes) // gemm.input_dtype(family).itemsize + 64 * 64
-        max_a = max(floor, max(p.batch * p.m * p.k for p in problems))
-        max_b = max(floor, max(p.batch * p.k * p.n for p in problems))
-        max_c = max(floor, max(p.batch * p.m * p.n for p in problems))
+        al = 16 // dtype.itemsize  # pitched rows (operands())
+        max_a = max(floor, max(p.batch * p.m * -(-p.k // al) * al for p in problems))
+        max_b = max(floor, max(p.batch * p.k * -(-p.n // al) * al for p in problems))
+        max_c = max(floor, max(p.batch * p.m * -(-p.n // 4) * 4 for p in problems))
         gen = torch.Generator(device=self.device).manual_seed(seed)
         self.bufA = (torch.rand(max_a, device=self.device, generator=gen) * 2 - 1).to(dtype)
         self.bufB = (torch.rand(max_b, device=self.device, generator=gen) * 2 - 1).to(dtype)
@@ -133,10 +134,15 @@ class CudaEventTimer:
             return "", ""
 
     def operands(self, problem: ProblemSize):
-        """Operand sets for the problem: one, or enough copies to cover 2 x L2."""
+        """Operand sets for the problem: one, or enough copies to cover 2 x L2.  Rows are
+        pitched to 16 bytes (leading dimensions rounded up to 16 bytes of elements, as
+        cudaMallocPitch / the VGG16 im2col writes them), so ragged k or n (27, 147, ...)
+        keep the TMA operand paths; the GEMM itself is the problem's m x k x n."""
         if self._ops_key != problem:
             p = problem
-            na, nb, nc = p.batch * p.m * p.k, p.batch * p.k * p.n, p.batch * p.m * p.n
+            al = 16 // self.bufA.element_size()
+            lda, ldb, ldc = -(-p.k // al) * al, -(-p.n // al) * al, -(-p.n // 4) * 4
+            na, nb, nc = p.batch * p.m * lda, p.batch * p.k * ldb, p.batch * p.m * ldc
             foot = na * self.bufA.element_size() + nb * self.bufB.element_size() + nc * 4
             sets = 1 if foot >= 2 * self.l2_bytes else math.ceil(2 * self.l2_bytes / foot)
             pad = lambda x: (x + 63) // 64 * 64  # noqa: E731  (256-byte aligned copies)
@@ -144,9 +150,9 @@ class CudaEventTimer:
                               self.bufC.numel() // pad(nc)))
             ops = []
             for i in range(sets):
-                A = self.bufA[i * pad(na): i * pad(na) + na].view(p.batch, p.m, p.k)
-                B = self.bufB[i * pad(nb): i * pad(nb) + nb].view(p.batch, p.k, p.n)
-                C = self.bufC[i * pad(nc): i * pad(nc) + nc].view(p.batch, p.m, p.n)
+                A = self.bufA[i * pad(na): i * pad(na) + na].view(p.batch, p.m, lda)[:, :, :p.k]
+                B = self.bufB[i * pad(nb): i * pad(nb) + nb].view(p.batch, p.k, ldb)[:, :, :p.n]
+                C = self.bufC[i * pad(nc): i * pad(nc) + nc].view(p.batch, p.m, ldc)[:, :, :p.n]
                 ops.append(self.gemm.GemmOperands(A, B, C, A.dtype))
             self._ops = ops
             self._ops_key = problem
@@ -344,11 +350,16 @@ def write_benchmark_csv(pm: PerfMatrix, path: str | os.PathLike) -> None:
 
 
 def problem_set(name: str, batches=(1, 2, 4, 8, 16, 32, 64)) -> list[ProblemSize]:
-    """Named sweep shape sets: vgg16 / resnet50 (conv-as-GEMM x batches), square, square16k."""
+    """Named sweep shape sets: vgg16 / resnet50 (conv-as-GEMM x batches), vgg16+paper
+    (vgg16 then the paper's three sample problems, shapes.PAPER_SAMPLES), square,
+    square16k."""
     from . import shapes
 
     if name in shapes.NETWORKS:
         return shapes.network_problems(name, batches)
+    if name == "vgg16+paper":
+        rows = shapes.network_problems("vgg16", batches)
+        return rows + [p for p in shapes.PAPER_SAMPLES if p not in rows]
     if name == "square":  # 64..8192 squares + skinny extremes (full 640-config families)
         return shapes.square_skinny_problems(sizes=(64, 128, 256, 512, 1024, 2048, 4096, 8192))
     if name == "square16k":  # adds 16384^3 (tensor-core families)
@@ -369,7 +380,8 @@ def main(argv=None) -> int:
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--out", required=True, help="benchmark CSV (reference format)")
     ap.add_argument("--work", default=None, help="shard/partial directory (default: <out>.parts)")
-    ap.add_argument("--min-ms", type=float, default=3.0)
+    ap.add_argument("--min-ms", type=float, default=60.0,
+                    help="timed ms per cell, split over 3 loops (SURVEY 8(d): loops >= 20 ms)")
     args = ap.parse_args(argv)
     problems = problem_set(args.set, tuple(int(b) for b in args.batches.split(",")))
     work = Path(args.work or (args.out + ".parts"))

@@ -20,7 +20,7 @@ import math
 
 import torch
 
-from . import _lib
+from . import _lib, gemm
 from .dataset import ProblemSize
 
 # (Cin, Cout) per conv, "M" = 2x2 max pool (configuration D).
@@ -51,8 +51,11 @@ def init_weights(seed: int = 0, device="cpu"):
 class Vgg16:
     """Preallocated VGG16 forward for a fixed batch on one device."""
 
-    def __init__(self, dispatcher, batch: int, device, seed: int = 0, weights=None):
+    def __init__(self, dispatcher, batch: int, device, seed: int = 0, weights=None, implicit: bool = True):
         self.disp = dispatcher
+        # implicit: conv layers whose dispatched SIMT variant supports it run as implicit
+        # GEMMs (kp_conv3x3_nhwc_ex, TMA im2col) instead of im2col + GEMM
+        self.implicit = implicit
         self.batch = batch
         self.device = torch.device(device)
         convs, fcs = weights if weights is not None else init_weights(seed)
@@ -120,6 +123,16 @@ class Vgg16:
                 w, b = self.convs[ci]
                 ci += 1
                 m, k = B * H * H, 9 * cin
+                vid = self.disp.variant(ProblemSize(m, k, cout, 1))
+                if self.implicit and not self.bf16 and gemm.conv3x3_supported(vid, cin, cout):
+                    # implicit GEMM: TMA im2col copies gather the patches from src directly
+                    _lib.check(lib.kp_conv3x3_nhwc_ex(vid, src.data_ptr(), B, H, H, cin, w.data_ptr(), cout,
+                                                      dst.data_ptr(), b.data_ptr(), _lib.KP_EPI_RELU, stream_handle),
+                               f"kp_conv3x3_nhwc_ex({B}x{H}x{H}x{cin} -> {cout})")
+                    C = cout
+                    src = dst
+                    dst_i ^= 1
+                    continue
                 if self.bf16:
                     k = k if k % 8 == 0 else self.k_pad0
                     _lib.check(lib.kp_im2col3x3_nhwc_bf16(src.data_ptr(), B, H, H, cin, self.cols.data_ptr(), k,

@@ -169,3 +169,16 @@ def test_simt_staging_switch(lib):
     assert lib.kp_set_simt_staging(-1) == _lib.KP_EINVAL
     with pytest.raises(ValueError):
         gemm.set_simt_staging("ldgsts")
+
+
+def test_conv3x3_supported_query(lib):
+    """kp_conv3x3_supported needs no GPU: SIMT variants with TMA staging and C a multiple
+    of their k-tile depth; never the paper / tensor-core families; bad ids -ENOENT."""
+    from paper_2008_13145_b200 import gemm
+    vid = gemm.variant_id(KernelConfig(8, 8, 8, 16, 8), "simt")
+    assert lib.kp_conv3x3_supported(vid, 64, 64) == 1
+    assert lib.kp_conv3x3_supported(vid, 3, 64) == 0
+    assert lib.kp_conv3x3_supported(vid, 64, 62) == 0
+    assert lib.kp_conv3x3_supported(gemm.variant_id(KernelConfig(8, 8, 8, 1, 128), "simt"), 64, 64) == 0  # BN 1024
+    assert lib.kp_conv3x3_supported(gemm.variant_id(KernelConfig(8, 8, 8, 16, 8), "paper"), 64, 64) == 0
+    assert lib.kp_conv3x3_supported(10 ** 6, 64, 64) == _lib.KP_ENOENT

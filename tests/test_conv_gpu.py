@@ -1,0 +1,78 @@
+"""GPU: the implicit-GEMM 3x3 convolution (kp_conv3x3_nhwc_ex -- TMA im2col copies
+straight from the NHWC activation) equals im2col + the same GEMM variant bit for bit,
+and both equal the oracle (numpy im2col + the fmaf chain of the launch's k-slice plan),
+for every SIMT config that supports it; shapes whose pixel runs cross image rows and
+images, ragged m tails, fused bias + ReLU."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import gemm_oracle as go
+from oracle import vgg16_ref
+from paper_2008_13145_b200 import _lib, gemm
+from paper_2008_13145_b200.dataset import KernelConfig, ProblemSize, enumerate_configs
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(x):
+    return np.ascontiguousarray(x).view(np.uint32)
+
+
+@pytest.mark.parametrize("B,H,W,C,cout", [(2, 9, 7, 32, 64), (1, 14, 14, 64, 128), (3, 5, 6, 16, 48)])
+def test_implicit_conv_all_configs_bit_exact(cuda_device, B, H, W, C, cout):
+    rng = np.random.default_rng(B * 100 + C)
+    x = rng.standard_normal((B, H, W, C)).astype(np.float32)
+    w = (rng.standard_normal((9 * C, cout)) * 0.1).astype(np.float32)
+    bias = (rng.standard_normal(cout) * 0.1).astype(np.float32)
+    dx, dw, db = (torch.from_numpy(a).to(cuda_device) for a in (x, w, bias))
+    cols = torch.from_numpy(vgg16_ref.im2col3x3(x)).to(cuda_device)
+    prob = ProblemSize(B * H * W, 9 * C, cout, 1)
+    lib = _lib.load()
+    checked, bad, cache = 0, [], {}
+    for cfg in enumerate_configs():
+        vid = gemm.variant_id(cfg, "simt")
+        if not gemm.conv3x3_supported(vid, C, cout):
+            continue
+        got = gemm.conv3x3(dx, dw, vid, bias=db, relu=True).cpu().numpy().reshape(-1, cout)
+        ref = torch.empty(prob.m, cout, device=cuda_device)
+        assert lib.kp_gemm_ex(vid, prob.m, prob.k, cout, 1, cols.data_ptr(), prob.k, 0, dw.data_ptr(), cout, 0,
+                              ref.data_ptr(), cout, 0, db.data_ptr(), _lib.KP_EPI_RELU, None) == 0
+        kps = gemm.k_slice_plan(vid, prob)[1]
+        if kps not in cache:
+            y = go.gemm_sliced(vgg16_ref.im2col3x3(x), w, kps)[0]
+            cache[kps] = _bits(np.maximum(y + bias, np.float32(0.0)))
+        if not (np.array_equal(_bits(got), _bits(ref.cpu().numpy())) and np.array_equal(_bits(got), cache[kps])):
+            bad.append(cfg.as_tuple())
+        checked += 1
+    assert checked > (300 if C % 32 == 0 else 60), checked
+    assert not bad, f"{len(bad)} configs differ, e.g. {bad[:5]}"
+
+
+def test_implicit_conv_rejects_ineligible(cuda_device):
+    lib = _lib.load()
+    vid = gemm.variant_id(KernelConfig(8, 8, 8, 16, 8), "simt")
+    x = torch.zeros(1, 8, 8, 3, device=cuda_device)
+    w = torch.zeros(27, 64, device=cuda_device)
+    out = torch.zeros(1, 8, 8, 64, device=cuda_device)
+    assert not gemm.conv3x3_supported(vid, 3, 64)  # C = 3 is not a multiple of the k-tile
+    assert lib.kp_conv3x3_nhwc_ex(vid, x.data_ptr(), 1, 8, 8, 3, w.data_ptr(), 64, out.data_ptr(), None, 0,
+                                  None) == _lib.KP_EINVAL
+    with pytest.raises(ValueError):
+        gemm.conv3x3(x, w[:26], vid)
+
+
+def test_implicit_conv_large_layer_matches_explicit(cuda_device):
+    """VGG16 conv3_2 at batch 4 (m = 12544, k = 2304): implicit == explicit, bitwise."""
+    g = torch.Generator(device=cuda_device).manual_seed(3)
+    x = torch.randn(4, 56, 56, 256, device=cuda_device, generator=g)
+    w = torch.randn(9 * 256, 256, device=cuda_device, generator=g) * 0.02
+    lib = _lib.load()
+    cols = torch.empty(4 * 56 * 56, 9 * 256, device=cuda_device)
+    assert lib.kp_im2col3x3_nhwc(x.data_ptr(), 4, 56, 56, 256, cols.data_ptr(), 9 * 256, None) == 0
+    for cfg in (KernelConfig(8, 8, 8, 16, 8), KernelConfig(8, 1, 8, 8, 16), KernelConfig(4, 2, 8, 16, 8)):
+        vid = gemm.variant_id(cfg, "simt")
+        got = gemm.conv3x3(x, w, vid).reshape(-1, 256)
+        want = gemm.matmul(cols, w, cfg, "simt")
+        assert torch.equal(got.view(torch.int32), want.view(torch.int32)), cfg
