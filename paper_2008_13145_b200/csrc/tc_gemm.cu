@@ -19,7 +19,8 @@
 //
 // Config 5-tuple of these families (include/kpgemm.h KernelChoice), documented in
 // (tile_rows, tile_acc, tile_cols, wg_rows, wg_cols) =
-//   (BM = 128, BK = elements per 128-byte K slab, BN, STAGES, threads = 192).
+//   (BM = 128, or 256 for CTA pairs, BK = elements per 128-byte K slab, BN, STAGES,
+//    threads per CTA = 192).
 //
 // Operands whose rows are not 16-byte aligned (TMA's requirement; e.g. VGG conv1_1
 // k = 27, ResNet conv1 k = 147) are staged by the epilogue warps with ordinary loads
@@ -483,6 +484,283 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (sliced) tc_slice_reduce<BN>(p, reinterpret_cast<float*>(smem), tiles_m, tiles_n, tile_begin);
 }
 
+// ------------------------------------------------------- CTA pairs (2-CTA MMA) --
+// tcgen05.mma.cta_group::2: a (2, 1, 1) cluster -- two SMs of one TPC -- computes a
+// 256 x BN tile.  Each CTA stages its own 128 rows of A and its own BN/2 columns of B
+// (so each operand byte is loaded by one SM only and each SM's shared memory feeds
+// half the B panel), the leader CTA issues M = 256 MMAs that read both CTAs' stages,
+// and each CTA's TMEM receives its 128 rows x BN fp32 accumulator.  Barriers:
+//   full[s]       leader only: one arrive.expect_tx for both CTAs' bytes; both CTAs'
+//                 TMA copies complete_tx on it (.cta_group::2 signalling);
+//   empty[s]      both CTAs: the leader's tcgen05.commit multicasts to both;
+//   tmem_full[a]  both CTAs: commit multicast, each CTA's epilogue waits on its own;
+//   tmem_empty[a] leader only: 8 arrivals (4 epilogue warps per CTA, the peer's remote).
+// Persistent over tile pairs; TMA operands only (the launcher falls back to the 1-CTA
+// kernel for LSU staging and k-sliced launches).
+constexpr int BM2 = 256;
+
+template <bool kTF32, int BN, int STAGES>
+struct Tc2Cfg {
+  using Base = TcCfg<kTF32, BN, 2>;  // stage-independent facts (BK, UK, NATOM, TMEM columns)
+  static constexpr int ES = Base::ES, BK = Base::BK, UK = Base::UK, NATOM = Base::NATOM;
+  static constexpr int BNH = BN / 2;                     // B columns staged per CTA
+  static constexpr int A_BYTES = BM * 128;               // this CTA's 128 rows of A
+  static constexpr int B_BYTES = BK * BNH * ES;          // this CTA's half of B
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = Base::TMEM_COLS;
+  static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
+  static constexpr int EPI_OFFSET = RING_BYTES + 1024;
+  static constexpr int EPI_BYTES = 4 * 2 * 32 * 32 * 4;
+  static constexpr int SMEM_BYTES = EPI_OFFSET + EPI_BYTES + 1024;
+  static constexpr uint32_t IDESC = (1u << 4) | ((kTF32 ? 2u : 1u) << 7) | ((kTF32 ? 2u : 1u) << 10) | (0u << 15) |
+                                    (1u << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                                    (static_cast<uint32_t>(BM2 >> 4) << 24);
+  static_assert(BNH % NATOM == 0, "each CTA stages whole swizzle atoms of B");
+  static_assert(SMEM_BYTES <= 227 * 1024, "smem");
+};
+
+// mbarrier wait that traps after ~2^28 polls (seconds) instead of hanging the GPU if a
+// pair's protocol ever loses an arrival: a trapped kernel fails its launch cleanly.
+__device__ __forceinline__ void mbar_wait_pair(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t polls = 0; !done; ++polls) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (polls > (1u << 28)) __trap();
+  }
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of this CTA's variable at `p` as seen in CTA `rank`
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int x, int y,
+                                                 int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_cluster), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+template <bool kTF32>
+__device__ __forceinline__ void mma_issue_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accum) {
+  if constexpr (kTF32) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  } else {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  }
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+__device__ __forceinline__ void tile_coords_pair(int t, int tiles_m, int tiles_n, int bn, int& b, int& m0, int& n0) {
+  const int per_batch = tiles_m * tiles_n;
+  b = t / per_batch;
+  const int r = t - b * per_batch;
+  const int band = r / (kGroupM * tiles_n);
+  const int first = band * kGroupM;
+  const int rows = tiles_m - first < kGroupM ? tiles_m - first : kGroupM;
+  const int local = r - band * kGroupM * tiles_n;
+  m0 = (first + local % rows) * BM2;
+  n0 = (local / rows) * bn;
+}
+
+template <bool kTF32, int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc2_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                    const __grid_constant__ CUtensorMap mapC, GemmArgs p, int tiles_m, int tiles_n, int a_batched,
+                    int b_batched, int tma_store) {
+  using Cfg = Tc2Cfg<kTF32, BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::RING_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int KT = (p.k + Cfg::BK - 1) / Cfg::BK;
+  const int n_tiles = tiles_m * tiles_n * p.batch;  // 256-row tiles
+  const int pair = static_cast<int>(blockIdx.x) >> 1, pairs = static_cast<int>(gridDim.x) >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 8);  // 4 epilogue warps in each CTA of the pair
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs; completions land on the leader) ----------------
+    int it = 0;
+    for (int t = pair; t < n_tiles; t += pairs) {
+      int b, m0, n0;
+      tile_coords_pair(t, tiles_m, tiles_n, BN, b, m0, n0);
+      const int za = a_batched ? b : 0, zb = b_batched ? b : 0;
+      for (int kt = 0; kt < KT; ++kt, ++it) {
+        const int s = it % STAGES;
+        mbar_wait_pair(&empty[s], ((it / STAGES) & 1) ^ 1);
+        uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
+        uint8_t* sb = sa + Cfg::A_BYTES;
+        const uint32_t fbar = map_rank(&full[s], 0);
+        if (leader) mbar_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
+        tma_load_3d_pair(sa, &mapA, fbar, kt * Cfg::BK, m0 + static_cast<int>(rank) * BM, za);
+#pragma unroll
+        for (int j = 0; j < Cfg::BNH / Cfg::NATOM; ++j)
+          tma_load_3d_pair(sb + j * (Cfg::BK * 128), &mapB, fbar, n0 + static_cast<int>(rank) * Cfg::BNH + j * Cfg::NATOM,
+                           kt * Cfg::BK, zb);
+      }
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---------------- MMA issuer (leader only; M = 256 over both CTAs' stages) ----------------
+    int it = 0, i = 0;
+    for (int t = pair; t < n_tiles; t += pairs, ++i) {
+      const int a = i & 1;
+      mbar_wait_pair(&tmem_empty[a], ((i >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dtmem = tmem_base + a * BN;
+      for (int kt = 0; kt < KT; ++kt, ++it) {
+        const int s = it % STAGES;
+        mbar_wait_pair(&full[s], (it / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
+        const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < Cfg::BK / Cfg::UK; ++kk) {
+          const uint64_t adesc = smem_desc(sa + kk * 32, 16, 1024);
+          const uint64_t bdesc = kTF32 ? smem_desc(sb + kk * Cfg::UK * 128, Cfg::BK * 128, 512, 1)
+                                       : smem_desc(sb + kk * Cfg::UK * 128, Cfg::BK * 128, 1024, 2);
+          mma_issue_pair<kTF32>(dtmem, adesc, bdesc, Cfg::IDESC, (kt | kk) != 0);
+        }
+        mma_commit_pair(&empty[s]);
+      }
+      mma_commit_pair(&tmem_full[a]);
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue: this CTA's 128 rows of each 256-row tile ----------------
+    const int quad = warp & 3;
+    const uint32_t empty_bar0 = map_rank(&tmem_empty[0], 0), empty_bar1 = map_rank(&tmem_empty[1], 0);
+    int i = 0, epi_box = 0;
+    for (int t = pair; t < n_tiles; t += pairs, ++i) {
+      int b, m0, n0;
+      tile_coords_pair(t, tiles_m, tiles_n, BN, b, m0, n0);
+      m0 += static_cast<int>(rank) * BM;
+      const int a = i & 1;
+      mbar_wait_pair(&tmem_full[a], (i >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + quad * 32 + lane;
+      float* out = static_cast<float*>(p.C) + static_cast<int64_t>(b) * p.sC + static_cast<int64_t>(row) * p.ldc;
+      if (tma_store) {
+        uint8_t* stage = smem + Cfg::EPI_OFFSET + quad * (2 * 32 * 32 * 4);
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32, ++epi_box) {
+          float v[32];
+          tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * BN + c, v);
+          tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * BN + c + 16, v + 16);
+          if (p.bias || p.relu) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (n0 + c + e < p.n) v[e] = epilogue(p, v[e], n0 + c + e);
+          }
+          uint8_t* box = stage + (epi_box & 1) * (32 * 32 * 4);
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&mapC, box, n0 + c, m0 + quad * 32, b);
+            bulk_commit();
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 16) {
+          float v[16];
+          tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * BN + c, v);
+          if (row < p.m) {
+            const int col = n0 + c;
+            if (p.bias || p.relu) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (col + e < p.n) v[e] = epilogue(p, v[e], col + e);
+            }
+            if (p.c_vec && col + 16 <= p.n) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                *reinterpret_cast<float4*>(out + col + 4 * q) =
+                    make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (col + e < p.n) out[col + e] = v[e];
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a ? empty_bar1 : empty_bar0)
+                     : "memory");
+    }
+  }
+  if (warp >= 2 && lane == 0 && tma_store) bulk_wait_all();
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs done with TMEM and with each other's barriers
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
+  }
+}
+
 // ---------------------------------------------------------------- host side --
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -516,19 +794,24 @@ int num_sms() {
 struct TcConfig {
   bool tf32;
   int bn, stages;
+  int cg;  // 1: one CTA per 128-row tile; 2: CTA pairs (cta_group::2) per 256-row tile
 };
 
-// The family config lists (index order = the family's canonical column order).
-constexpr TcConfig kTf32Configs[] = {{true, 32, 4},  {true, 64, 4},  {true, 128, 4}, {true, 256, 4},
-                                     {true, 64, 8},  {true, 128, 6}, {true, 256, 3}, {true, 192, 4}};
-constexpr TcConfig kBf16Configs[] = {{false, 64, 4},  {false, 128, 4}, {false, 256, 4}, {false, 64, 8},
-                                     {false, 128, 6}, {false, 256, 3}, {false, 128, 2}, {false, 192, 4}};
-constexpr int kNumTc = 8;
+// The family config lists (index order = the family's canonical column order; the
+// first eight are round 1's, later entries append so measured tables keep their columns).
+constexpr TcConfig kTf32Configs[] = {{true, 32, 4, 1},  {true, 64, 4, 1},  {true, 128, 4, 1}, {true, 256, 4, 1},
+                                     {true, 64, 8, 1},  {true, 128, 6, 1}, {true, 256, 3, 1}, {true, 192, 4, 1},
+                                     {true, 96, 4, 1},  {true, 160, 4, 1}, {true, 256, 6, 2}, {true, 128, 8, 2},
+                                     {true, 192, 6, 2}};
+constexpr TcConfig kBf16Configs[] = {{false, 64, 4, 1},  {false, 128, 4, 1}, {false, 256, 4, 1}, {false, 64, 8, 1},
+                                     {false, 128, 6, 1}, {false, 256, 3, 1}, {false, 128, 2, 1}, {false, 192, 4, 1},
+                                     {false, 256, 6, 2}, {false, 128, 8, 2}, {false, 256, 4, 2}};
+constexpr int kNumTf32 = sizeof(kTf32Configs) / sizeof(kTf32Configs[0]);
+constexpr int kNumBf16 = sizeof(kBf16Configs) / sizeof(kBf16Configs[0]);
 
 const TcConfig* config_of(int family, int index) {
-  if (index < 0 || index >= kNumTc) return nullptr;
-  if (family == KP_FAMILY_TF32) return &kTf32Configs[index];
-  if (family == KP_FAMILY_BF16) return &kBf16Configs[index];
+  if (family == KP_FAMILY_TF32) return (index >= 0 && index < kNumTf32) ? &kTf32Configs[index] : nullptr;
+  if (family == KP_FAMILY_BF16) return (index >= 0 && index < kNumBf16) ? &kBf16Configs[index] : nullptr;
   return nullptr;
 }
 
@@ -538,7 +821,46 @@ bool tma_ok(const GemmArgs& p, int es) {
          (p.batch == 1 || ((p.sA * es) % 16 == 0 && (p.sB * es) % 16 == 0));
 }
 
+// A persistent CTA-pair launch over 256-row tiles (tc2_gemm_kernel).
 template <bool kTF32, int BN, int STAGES>
+cudaError_t launch_pair(const GemmArgs& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                        int a_batched, int b_batched, int tma_store, cudaStream_t s) {
+  using Cfg = Tc2Cfg<kTF32, BN, STAGES>;
+  static int fit = 0;  // co-resident pairs (cudaOccupancyMaxActiveClusters), per instantiation
+  cudaLaunchConfig_t lc = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  lc.stream = s;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  if (!fit) {
+    cudaError_t e = cudaFuncSetAttribute(tc2_gemm_kernel<kTF32, BN, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    lc.gridDim = dim3(2);
+    int n = 0;
+    e = cudaOccupancyMaxActiveClusters(&n, tc2_gemm_kernel<kTF32, BN, STAGES>, &lc);
+    if (e != cudaSuccess) return e;
+    if (n < 1) return cudaErrorInvalidConfiguration;
+    fit = n;
+  }
+  const int tiles_m = (p.m + BM2 - 1) / BM2, tiles_n = (p.n + BN - 1) / BN;
+  const int64_t n_tiles = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
+  if (n_tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  const int pairs = static_cast<int>(n_tiles < fit ? n_tiles : fit);
+  lc.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+  return cudaLaunchKernelEx(&lc, tc2_gemm_kernel<kTF32, BN, STAGES>, ma, mb, mc, p, tiles_m, tiles_n, a_batched,
+                            b_batched, tma_store);
+}
+
+// PAIR_STAGES > 0: a CTA-pair config -- persistent TMA launches run tc2_gemm_kernel with
+// that ring depth; LSU staging and k-sliced plans run the 1-CTA kernel (STAGES deep).
+template <bool kTF32, int BN, int STAGES, int PAIR_STAGES = 0>
 cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   using Cfg = TcCfg<kTF32, BN, STAGES>;
   static bool attr = false;
@@ -629,6 +951,12 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
         return cudaErrorInvalidValue;
     }
   }
+  if constexpr (PAIR_STAGES > 0) {
+    // CTA pairs for persistent TMA launches (no tail split: the pair kernel runs every tile)
+    if (!lsu && p.kslices <= 1)
+      return launch_pair<kTF32, BN, PAIR_STAGES>(p, ma, mb, mc, a_batched, b_batched, tma_store, s);
+    tail = 0;
+  }
   // one launch over tiles [t0, t0 + count): persistent (slices == 1, grid <= SMs) or
   // k-sliced (grid (count, 1, slices) in (1, 1, slices) clusters)
   auto go = [&](GemmArgs q, int t0, int count, int slices) -> cudaError_t {
@@ -703,14 +1031,26 @@ int cluster_fit_tc(int slices) {
   return n;
 }
 
+// 1-CTA (BN, STAGES) of a config: pair configs fall back to their 1-CTA twin (the
+// deepest ring that fits one SM) for LSU staging and k-sliced launches.
+constexpr int twin_stages(const TcConfig& c) {
+  return c.cg == 1 ? c.stages : (c.bn == 256 ? 3 : c.bn == 192 ? 4 : 6);
+}
+
 template <bool kTF32>
 int dispatch_fit(const TcConfig& c, int slices) {
-  switch (c.bn * 16 + c.stages) {
+  switch (c.bn * 16 + twin_stages(c)) {
     case 32 * 16 + 4:
       if constexpr (kTF32) return cluster_fit_tc<kTF32, 32, 4>(slices);
       return -1;
     case 64 * 16 + 4: return cluster_fit_tc<kTF32, 64, 4>(slices);
+    case 96 * 16 + 4:
+      if constexpr (kTF32) return cluster_fit_tc<kTF32, 96, 4>(slices);
+      return -1;
     case 128 * 16 + 4: return cluster_fit_tc<kTF32, 128, 4>(slices);
+    case 160 * 16 + 4:
+      if constexpr (kTF32) return cluster_fit_tc<kTF32, 160, 4>(slices);
+      return -1;
     case 256 * 16 + 4: return cluster_fit_tc<kTF32, 256, 4>(slices);
     case 64 * 16 + 8: return cluster_fit_tc<kTF32, 64, 8>(slices);
     case 128 * 16 + 6: return cluster_fit_tc<kTF32, 128, 6>(slices);
@@ -725,12 +1065,31 @@ int dispatch_fit(const TcConfig& c, int slices) {
 
 template <bool kTF32>
 cudaError_t dispatch(const TcConfig& c, const GemmArgs& p, cudaStream_t s) {
+  if (c.cg == 2) {
+    switch (c.bn * 16 + c.stages) {
+      case 256 * 16 + 6: return launch_tc<kTF32, 256, 3, 6>(p, s);
+      case 128 * 16 + 8: return launch_tc<kTF32, 128, 6, 8>(p, s);
+      case 256 * 16 + 4:
+        if constexpr (!kTF32) return launch_tc<kTF32, 256, 3, 4>(p, s);
+        return cudaErrorInvalidValue;
+      case 192 * 16 + 6:
+        if constexpr (kTF32) return launch_tc<kTF32, 192, 4, 6>(p, s);
+        return cudaErrorInvalidValue;
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (c.bn * 16 + c.stages) {
     case 32 * 16 + 4:
       if constexpr (kTF32) return launch_tc<kTF32, 32, 4>(p, s);
       return cudaErrorInvalidValue;
     case 64 * 16 + 4: return launch_tc<kTF32, 64, 4>(p, s);
+    case 96 * 16 + 4:
+      if constexpr (kTF32) return launch_tc<kTF32, 96, 4>(p, s);
+      return cudaErrorInvalidValue;
     case 128 * 16 + 4: return launch_tc<kTF32, 128, 4>(p, s);
+    case 160 * 16 + 4:
+      if constexpr (kTF32) return launch_tc<kTF32, 160, 4>(p, s);
+      return cudaErrorInvalidValue;
     case 256 * 16 + 4: return launch_tc<kTF32, 256, 4>(p, s);
     case 64 * 16 + 8: return launch_tc<kTF32, 64, 8>(p, s);
     case 128 * 16 + 6: return launch_tc<kTF32, 128, 6>(p, s);
@@ -745,12 +1104,14 @@ cudaError_t dispatch(const TcConfig& c, const GemmArgs& p, cudaStream_t s) {
 
 }  // namespace
 
-int tc_family_size(int family) { return (family == KP_FAMILY_TF32 || family == KP_FAMILY_BF16) ? kNumTc : 0; }
+int tc_family_size(int family) {
+  return family == KP_FAMILY_TF32 ? kNumTf32 : family == KP_FAMILY_BF16 ? kNumBf16 : 0;
+}
 
 KernelChoice tc_family_choice(int family, int index) {
   const TcConfig* c = config_of(family, index);
   if (!c) return KernelChoice{0, 0, 0, 0, 0};
-  return KernelChoice{BM, c->tf32 ? 32 : 64, c->bn, c->stages, kThreads};
+  return KernelChoice{BM * c->cg, c->tf32 ? 32 : 64, c->bn, c->stages, kThreads};
 }
 
 const char* tc_last_reason() { return g_reason; }

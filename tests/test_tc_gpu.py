@@ -139,3 +139,22 @@ def test_partial_last_wave_split(cuda_device, fam, m, k, n, batch):
     B = (torch.rand(k, n, device=cuda_device, generator=g) - 0.5).to(dt)
     cfg = gemm.family_configs(fam)[2]
     assert torch.equal(gemm.matmul(A, B, cfg, fam), gemm.matmul(A, B, cfg, fam))
+
+
+@pytest.mark.parametrize("fam", ["bf16", "tf32"])
+@pytest.mark.parametrize("m,k,n,batch", [(256, 256, 256, 1), (300, 520, 392, 1), (1000, 576, 256, 2),
+                                         (2048, 2048, 2048, 1), (4096, 1024, 4096, 1), (3136, 4608, 512, 1),
+                                         (700, 64, 1000, 1)])
+def test_cta_pair_configs(cuda_device, fam, m, k, n, batch):
+    """tile_rows = 256 configs run CTA pairs (tcgen05.mma.cta_group::2, each SM staging
+    half the operands) on persistent TMA launches: within the bound on ragged m/n tails
+    (a pair's second CTA partly or wholly past m), batches and long k; deterministic."""
+    pairs = [c for c in gemm.family_configs(fam) if c.tile_rows == 256]
+    assert len(pairs) >= 3
+    for cfg in pairs:
+        _check(fam, cfg, m, k, n, batch, cuda_device, bcast=(batch > 1), seed=m + k)
+    g = torch.Generator(device=cuda_device).manual_seed(5)
+    dt = torch.bfloat16 if fam == "bf16" else torch.float32
+    A = (torch.rand(m, k, device=cuda_device, generator=g) - 0.5).to(dt)
+    B = (torch.rand(k, n, device=cuda_device, generator=g) - 0.5).to(dt)
+    assert torch.equal(gemm.matmul(A, B, pairs[0], fam), gemm.matmul(A, B, pairs[0], fam))
