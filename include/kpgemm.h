@@ -57,12 +57,14 @@ extern "C" {
  * table: the oracle-best denominator spans every column of a table
  * (evaluate.py:81), so families are never mixed in one table silently. */
 #define KP_FAMILY_PAPER 0 /* F0: paper-faithful fp32 SIMT, no shared memory */
-#define KP_FAMILY_SIMT 1  /* F1: B200 fp32 SIMT, cp.async multi-stage smem pipeline, warp tiles   */
+#define KP_FAMILY_SIMT 1  /* F1: B200 fp32 SIMT, TMA/mbarrier (or cp.async) smem ring, warp tiles   */
 #define KP_FAMILY_TF32 2  /* F2: tcgen05 kind::tf32, fp32 in / fp32 out                            */
 #define KP_FAMILY_BF16 3  /* F3: tcgen05 kind::f16, bf16 in / fp32 out                              */
 #define KP_NUM_FAMILIES 4
 
-/* Field order is the emitted selector's (codegen.py:191-192). */
+/* Field order is the emitted selector's (codegen.py:191-192).  PAPER / SIMT families:
+ * the paper's meaning below (dataset.py:39-58).  TF32 / BF16 families: (BM = 128, or 256
+ * for CTA-pair configs, BK = elements per 128-byte k slab, BN, smem stages, 192 threads). */
 typedef struct KernelChoice {
   int32_t tile_rows; /* R: output rows per work item              */
   int32_t tile_acc;  /* A: accumulation depth per step / k vector */
