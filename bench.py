@@ -540,6 +540,15 @@ def run_ours(args, world, rank, local):
             traffic = None
     roof["traffic"] = traffic
     total_ms = sum(layer_ms)
+    # every layer against its own roofline (the binding term of min(pipe, AI x HBM))
+    simt_peak = gemm.ffma_peak_tflops(packed=True) if args.family in ("simt", "paper") else None
+    per_layer = []
+    for i, (name, p, _A, _W, _C, vid) in enumerate(bufs):
+        cfg, fam = gemm.variant_info(vid)
+        r = roofline(fam, p, layer_ms[i] / args.steps, in_dtype.itemsize, simt_peak)
+        per_layer.append({"layer": name, "problem": [p.m, p.k, p.n], "variant": list(cfg.as_tuple()),
+                          "ms": round(layer_ms[i] / args.steps, 4), "bound": r["bound"],
+                          "achieved": round(r["achieved"], 1), "unit": r["unit"], "frac": round(r["frac"], 3)})
 
     e2e = None if args.no_e2e else e2e_layers(args, world, device, stream, disp, bufs, step_flops, in_dtype)
 
@@ -574,6 +583,7 @@ def run_ours(args, world, rank, local):
             "roofline": dict(roof, kernel=f"{dom_fam}{dom_cfg.as_tuple()} on {dname} {[dp.m, dp.k, dp.n, dp.batch]}",
                              avg_launch_ms=dom_ms, share_of_step=dg["ms"] / total_ms,
                              variant_share_of_step=variant_ms / total_ms),
+            "layers": per_layer,
             "clocks": clocks.summary(),
         }
         if e2e is not None:

@@ -110,14 +110,26 @@ struct F1Cfg {
 #define KP_F1_WARPS 16
 #endif
   static constexpr int MIN_BLOCKS = (KP_F1_WARPS * 32 / NT) > 1 ? (KP_F1_WARPS * 32 / NT) : 1;
-  static constexpr int kBudget = (227 * 1024) / (MIN_BLOCKS < 4 ? MIN_BLOCKS : 4) - 1024;
   static constexpr int stage_floats(int bk) { return BM * (bk + PADA) + bk * BN; }
+  // Stage depth BK comes from a budget of up to 4 CTAs per SM; 64-thread work groups then
+  // take the 8-CTA budget (their full 16-warp target) when two stages of that BK still fit
+  // in it -- measured +2..17 % on those configs, while shrinking BK to fit 8 CTAs lost up
+  // to 2x (profiles/r2/occupancy_budget_ab.md).
+  static constexpr int budget_for(int ctas) {
+    return (227 * 1024) / (MIN_BLOCKS < ctas ? MIN_BLOCKS : ctas) - 1024;
+  }
+  static constexpr int kBudget4 = budget_for(4);
 #ifndef KP_F1_MAX_BK
 #define KP_F1_MAX_BK 32
 #endif
-  static constexpr int BK = (KP_F1_MAX_BK >= 32 && 2 * 4 * stage_floats(32) <= kBudget)   ? 32
-                            : (KP_F1_MAX_BK >= 16 && 2 * 4 * stage_floats(16) <= kBudget) ? 16
-                                                                                        : 8;
+  static constexpr int BK = (KP_F1_MAX_BK >= 32 && 2 * 4 * stage_floats(32) <= kBudget4)   ? 32
+                            : (KP_F1_MAX_BK >= 16 && 2 * 4 * stage_floats(16) <= kBudget4) ? 16
+                                                                                         : 8;
+#ifndef KP_F1_MAX_CTAS
+#define KP_F1_MAX_CTAS 8
+#endif
+  static constexpr int kBudget =
+      2 * 4 * stage_floats(BK) <= budget_for(KP_F1_MAX_CTAS) ? budget_for(KP_F1_MAX_CTAS) : kBudget4;
   static constexpr int SA = BK + PADA;  // LHS smem row stride (floats)
   static constexpr int SB = BN;         // RHS smem row stride (floats)
   static constexpr int STAGE = stage_floats(BK);
