@@ -108,7 +108,8 @@ int kp_gemm_ex(int id, int m, int k, int n, int batch,
  * consecutive slices, computed by the CTAs of one (1, 1, S) thread-block cluster per
  * output tile and summed in slice order ((p0 + p1) + p2) + ... through distributed
  * shared memory -- deterministic for a given (config, shape, device).
- *   SIMT:   u = output tiles / SMs; S = 8 (u < 0.5), 4 (u < 2), 2 (u < 6), else 1,
+ *   SIMT:   u = output tiles / SMs; S = 16 (u < 0.15, a non-portable cluster), 8 (u < 0.5),
+ *           4 (u < 2), 2 (u < 6), else 1,
  *           halved while the sliced grid exceeds 4 waves of resident CTAs, and never
  *           shallower than 64 in k (a rule fitted on measured forced-S data).
  *   TF32/BF16 (persistent 1-CTA/SM kernel): grids filling at most half the SMs,
@@ -125,7 +126,7 @@ int kp_gemm_ex(int id, int m, int k, int n, int batch,
  * device with that many SMs and no cluster limit).  kp_set_max_k_slices caps S
  * (1 disables slicing: every SIMT output is then the single fp32 fma chain over k,
  * bit-identical to the PAPER family, and the tensor-core families run persistent);
- * returns the previous cap (default 8, range 1..16). */
+ * returns the previous cap (default 16, range 1..16; the tensor-core rules never exceed 8). */
 int kp_set_max_k_slices(int max_slices);
 int kp_gemm_plan(int id, int m, int k, int n, int batch, int num_sms, int* k_slices, int* k_per_slice);
 

@@ -192,9 +192,11 @@ void plan_slices(int id, int m, int k, int n, int batch, int sms, bool device, i
       // Tiles per SM -> slices, fitted on 673 measured (shape, config) cells with every
       // forced S (profiles/r1_kslicing.md): u < 0.5 -> 8, < 2 -> 4, < 6 -> 2, else 1;
       // halved while the sliced grid would exceed 4 waves of resident CTAs, and never
-      // shallower than 64 in k.
+      // shallower than 64 in k.  Round 2 (TMA staging, 784 cells x S in 1..8,10,12,16,
+      // profiles/r2/kslice_refit.md): grids under 0.15 tiles per SM take 16-CTA
+      // (non-portable) clusters -- 0.952 -> 0.974 of the per-cell best S.
       const double u = static_cast<double>(tiles) / sms;
-      s = u < 0.5 ? 8 : u < 2.0 ? 4 : u < 6.0 ? 2 : 1;
+      s = u < 0.15 ? 16 : u < 0.5 ? 8 : u < 2.0 ? 4 : u < 6.0 ? 2 : 1;
       while (s > 1 && tiles * s > 4LL * sms * t.occ) s /= 2;
       if (s > max_slices) s = max_slices;
       if (s > k / kMinSliceK) s = k / kMinSliceK;
@@ -204,7 +206,8 @@ void plan_slices(int id, int m, int k, int n, int batch, int sms, bool device, i
       // persistent tensor-core kernel: slice only grids that fill at most half the SMs,
       // in one wave of clusters (a second wave of non-persistent CTAs loses to it)
       const int64_t want = static_cast<int64_t>(sms) * t.occ / tiles;
-      s = static_cast<int>(want < max_slices ? want : max_slices);
+      const int cap = max_slices < kp::kPortableKSlices ? max_slices : kp::kPortableKSlices;
+      s = static_cast<int>(want < cap ? want : cap);
       const int by_k = k / kMinSliceKTc;
       if (s > by_k) s = by_k;
       if (s < 1) s = 1;
@@ -218,7 +221,8 @@ void plan_slices(int id, int m, int k, int n, int batch, int sms, bool device, i
       const int64_t r = tiles % sms;
       const int64_t work = static_cast<int64_t>(t.bn) * k * (v.family == KP_FAMILY_TF32 ? 2 : 1);
       if (r > 0 && 2 * r <= sms && k >= 2 * kMinSliceKTc && work >= 1720000) {
-        int ts = static_cast<int>(sms / r < max_slices ? sms / r : max_slices);
+        const int cap = max_slices < kp::kPortableKSlices ? max_slices : kp::kPortableKSlices;
+        int ts = static_cast<int>(sms / r < cap ? sms / r : cap);
         if (ts > k / kMinSliceKTc) ts = k / kMinSliceKTc;
         if (device && ts > 1) ts = fit_slices(id, v, ts, r);
         if (ts > 1) {

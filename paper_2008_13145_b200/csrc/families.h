@@ -33,7 +33,8 @@ struct F1Entry {
 extern std::atomic<int> g_f1_tma_staging;
 
 constexpr int kMaxKSlices = 16;      // non-portable thread-block-cluster limit on sm_100
-constexpr int kDefaultKSlices = 8;   // portable clusters: measured faster than 9..16
+constexpr int kDefaultKSlices = 16;  // cap of kp_set_max_k_slices; the planner's rules pick S
+constexpr int kPortableKSlices = 8;  // tensor-core families: portable clusters measured faster than 9..16
 
 // F0 (family PAPER): any (R,A,C) in {1,2,4,8}^3, any block shape <= 1024 threads.
 cudaError_t f0_launch(const KernelChoice& ch, GemmArgs p, cudaStream_t s);

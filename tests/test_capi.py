@@ -122,7 +122,7 @@ def test_dispatch_load_rejects_malformed_trees(lib):
 
 def test_k_slice_plan_host_logic(lib):
     """kp_gemm_plan with an explicit SM count needs no GPU.  SIMT rule (fitted on measured
-    forced-S data): tiles per SM u < 0.5 -> 8 slices, < 2 -> 4, < 6 -> 2, else 1,
+    forced-S data): tiles per SM u < 0.15 -> 16 slices, < 0.5 -> 8, < 2 -> 4, < 6 -> 2, else 1,
     halved while the grid would exceed 4 waves of resident CTAs, never shallower than 64
     in k; no empty slice, k-tile aligned; the paper family and a cap of 1 never slice."""
     from paper_2008_13145_b200 import gemm
@@ -134,7 +134,7 @@ def test_k_slice_plan_host_logic(lib):
         tiles_m, tiles_n = cfg.tile_rows * cfg.wg_rows, cfg.tile_cols * cfg.wg_cols
         for p in probs:
             s, kps = gemm.k_slice_plan(cfg, p, num_sms=148)
-            assert 1 <= s <= 8  # 8/4/2, fewer when k has fewer k-tiles than that
+            assert 1 <= s <= 16  # 16/8/4/2, fewer when k has fewer k-tiles than that
             if s == 1:
                 assert kps == p.k
                 continue
@@ -143,7 +143,7 @@ def test_k_slice_plan_host_logic(lib):
             assert (s - 1) * kps < p.k <= s * kps  # no empty slice
             assert kps % 8 == 0  # a whole number of k-tiles (BK in {8, 16, 32})
             tiles = -(-p.m // tiles_m) * -(-p.n // tiles_n) * p.batch
-            assert tiles < (0.5 if s > 4 else 2 if s > 2 else 6) * 148  # tiles-per-SM bins
+            assert tiles < (0.15 if s > 8 else 0.5 if s > 4 else 2 if s > 2 else 6) * 148  # tiles-per-SM bins
         big = ProblemSize(16384, 4096, 16384, 1)
         assert gemm.k_slice_plan(cfg, big, num_sms=148) == (1, 4096)
         assert gemm.k_slice_plan(cfg, ProblemSize(1, 4096, 1, 1), family="paper", num_sms=148) == (1, 4096)
