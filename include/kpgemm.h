@@ -137,6 +137,17 @@ int kp_gemm_plan(int id, int m, int k, int n, int batch, int num_sms, int* k_sli
  * other value is -EINVAL. */
 int kp_set_simt_staging(int mode);
 
+/* Operands whose rows TMA cannot address (row pitch or base not 16-byte aligned, e.g. raw
+ * k = 27 im2col rows) on the TMA-staged families (SIMT configs that stage with TMA, TF32,
+ * BF16) are either copied into a 16-byte-pitched stream-ordered scratch first -- one
+ * HBM-bound pass -- and then take the TMA path, or staged in-kernel (SIMT: 4-byte
+ * cp.async; TF32/BF16: LSU loads into the swizzled ring).  mode 1 (default) repacks when
+ * the copy pays for itself (tensor cores: unaligned operands >= 4 MB or k > 4 k-tiles;
+ * SIMT: unaligned operands at least as large as the output), 2 always, 0 never.  Results
+ * are identical either way (SIMT: bit-identical).  Returns the previous mode; any other
+ * value is -EINVAL. */
+int kp_set_operand_repack(int mode);
+
 /* ---- benchmark harness ---------------------------------------------------
  * warmup untimed launches, then one launch timed alone to size the loop, then
  * max(min_iters, ceil(min_ms / t1)) (capped at max_iters) back-to-back launches

@@ -71,6 +71,7 @@ SIGNATURES = {
     "kp_gemm_ex": (_i, [_i] + _GEMM_ARGS + [_vp, _i, _vp]),
     "kp_set_max_k_slices": (_i, [_i]),
     "kp_set_simt_staging": (_i, [_i]),
+    "kp_set_operand_repack": (_i, [_i]),
     "kp_gemm_plan": (_i, [_i, _i, _i, _i, _i, _i, _ip, _ip]),
     "kp_bench": (_i, [_i] + _GEMM_ARGS + [_i, _i, _i, ctypes.c_double, _dp, _ip, _vp]),
     "kp_bench_sets": (_i, [_i, _i, _i, _i, _i, _i, _vpp, _i64, _i64, _vpp, _i64, _i64, _vpp, _i64, _i64,

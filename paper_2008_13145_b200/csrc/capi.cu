@@ -17,6 +17,7 @@
 #include "tc_families.h"
 
 std::atomic<int> kp::g_f1_tma_staging{1};  // kp_set_simt_staging
+std::atomic<int> g_operand_repack{1};      // kp_set_operand_repack
 
 namespace {
 
@@ -243,6 +244,97 @@ void plan_slices(int id, int m, int k, int n, int batch, int sms, bool device, i
   *bk = t.bk;
 }
 
+// ------------------------------------------------------- operand repacking --
+// TMA needs 16-byte-aligned operand rows.  Operands whose rows are not (raw k = 27 or
+// 147 im2col rows, n = 27, ...) are first copied into a 16-byte-pitched scratch copy --
+// one HBM-bound pass -- and the launch then takes the TMA path (the tensor-core families'
+// LSU staging measured 8 % of the HBM roofline on such rows; profiles/r2/repack.md).
+// Scratch is stream-ordered, from a library-owned pool per device that keeps up to 1 GiB
+// cached between launches (the process's default pool is left alone).
+cudaError_t scratch_alloc(void** ptr, size_t bytes, cudaStream_t s) {
+  static std::mutex mu;
+  static std::vector<cudaMemPool_t> pools;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaError_t e = cudaStreamIsCapturing(s, &cap); e != cudaSuccess) return e;
+  if (cap != cudaStreamCaptureStatusNone) return cudaMallocAsync(ptr, bytes, s);  // a graph memory node
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  cudaMemPool_t pool = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= static_cast<int>(pools.size())) pools.resize(dev + 1, nullptr);
+    if (!pools[dev]) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      if (cudaError_t e = cudaMemPoolCreate(&pools[dev], &props); e != cudaSuccess) return e;
+      uint64_t keep = 1ull << 30;
+      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool = pools[dev];
+  }
+  return cudaMallocFromPoolAsync(ptr, bytes, pool, s);
+}
+
+struct Repacked {
+  void* buf[2] = {nullptr, nullptr};
+  cudaStream_t s = nullptr;
+  ~Repacked() {
+    for (void* b : buf)
+      if (b) cudaFreeAsync(b, s);  // stream-ordered: after the GEMM that reads it
+  }
+};
+
+// Repack A and/or B of p (element size es) whose rows TMA cannot address, when the
+// copy pays for itself (measured, profiles/r2/repack.md):
+//   * tensor-core families: the in-kernel LSU staging runs at 8-30 % of the TMA path, so
+//     repack unless the unaligned operands are small (< 4 MB) and k spans at most 4 k-tiles
+//     (there the fixed cost of the extra pass loses: 12544 x 27 x 64 5.1 -> 3.8 TF/s);
+//   * SIMT: 4-byte cp.async staging is close to TMA when the output dominates the traffic
+//     (conv1_1: 20.8 TF/s in-kernel vs 19.4 with the repack pass), far behind it when the
+//     operands do (32 x 12321 x 27: 0.23 -> 0.56 TF/s), so repack only when the unaligned
+//     operands are at least as large as the output.
+cudaError_t repack_unaligned(kp::GemmArgs& p, int es, bool tensor_core, int bk, bool always, Repacked& rp,
+                             cudaStream_t s) {
+  auto rows_ok = [&](const void* ptr, int64_t ld, int64_t sb) {
+    return reinterpret_cast<uintptr_t>(ptr) % 16 == 0 && (ld * es) % 16 == 0 &&
+           (p.batch == 1 || sb == 0 || (sb * es) % 16 == 0);
+  };
+  const bool a_bad = !rows_ok(p.A, p.lda, p.sA), b_bad = !rows_ok(p.B, p.ldb, p.sB);
+  if (!a_bad && !b_bad) return cudaSuccess;
+  const int64_t nba = (p.batch > 1 && p.sA != 0) ? p.batch : 1, nbb = (p.batch > 1 && p.sB != 0) ? p.batch : 1;
+  const double bad_bytes = (a_bad ? static_cast<double>(nba) * p.m * p.k * es : 0.0) +
+                           (b_bad ? static_cast<double>(nbb) * p.k * p.n * es : 0.0);
+  const double out_bytes = static_cast<double>(p.batch) * p.m * p.n * 4.0;
+  const bool pays = tensor_core ? (bad_bytes >= 4.0 * (1 << 20) || p.k > 4 * bk) : bad_bytes >= out_bytes;
+  if (!pays && !always) return cudaSuccess;
+  rp.s = s;
+  const int al = 16 / es;
+  struct Op {
+    const void** ptr;
+    int64_t *ld, *sb;
+    int rows, cols;
+  } ops[2] = {{&p.A, &p.lda, &p.sA, p.m, p.k}, {&p.B, &p.ldb, &p.sB, p.k, p.n}};
+  for (int i = 0; i < 2; ++i) {
+    Op& o = ops[i];
+    if (rows_ok(*o.ptr, *o.ld, *o.sb)) continue;
+    const int nb = (p.batch > 1 && *o.sb != 0) ? p.batch : 1;
+    const int64_t ldd = (static_cast<int64_t>(o.cols) + al - 1) / al * al;
+    if (cudaError_t e = scratch_alloc(&rp.buf[i], static_cast<size_t>(nb) * o.rows * ldd * es, s); e != cudaSuccess) {
+      rp.buf[i] = nullptr;
+      return e;
+    }
+    if (cudaError_t e = kp::repack_rows_launch(*o.ptr, *o.ld, *o.sb, o.rows, o.cols, nb, es, rp.buf[i], ldd, s);
+        e != cudaSuccess)
+      return e;
+    *o.ptr = rp.buf[i];
+    *o.ld = ldd;
+    *o.sb = nb > 1 ? static_cast<int64_t>(o.rows) * ldd : 0;
+  }
+  return cudaSuccess;
+}
+
 int launch(int id, const kp::GemmArgs& p0, cudaStream_t s) {
   Registry& reg = registry();
   const Variant& v = reg.variants[id];
@@ -275,6 +367,18 @@ int launch(int id, const kp::GemmArgs& p0, cudaStream_t s) {
           p.kt_per_slice = (kt + forced - 1) / forced;
           p.kslices = (kt + p.kt_per_slice - 1) / p.kt_per_slice;
         }
+      }
+      // TMA-staged families: repack operand rows TMA cannot address (SIMT: only when this
+      // config stages with TMA; the implicit-conv path has its own operand contract)
+      Repacked rp;
+      const bool simt_tma = v.family == KP_FAMILY_SIMT && reg.f1[v.index].tma_ok && p.conv_c == 0 &&
+                            kp::g_f1_tma_staging.load(std::memory_order_relaxed) != 0;
+      if ((simt_tma || v.family != KP_FAMILY_SIMT) && g_operand_repack.load(std::memory_order_relaxed) != 0) {
+        const bool tc = v.family != KP_FAMILY_SIMT;
+        const int bk = tc ? kp::tc_tile_k(v.family) : reg.f1[v.index].bk;
+        e = repack_unaligned(p, v.family == KP_FAMILY_BF16 ? 2 : 4, tc, bk,
+                             g_operand_repack.load(std::memory_order_relaxed) == 2, rp, s);
+        if (e != cudaSuccess) return cuda_fail(e, "operand repack");
       }
       e = v.family == KP_FAMILY_SIMT ? reg.f1[v.index].launch(p, s) : kp::tc_launch(v.family, v.index, p, s);
       break;
@@ -429,6 +533,12 @@ int kp_set_max_k_slices(int max_slices) {
 int kp_set_simt_staging(int mode) {
   if (mode != 0 && mode != 1) return fail(KP_EINVAL, "staging mode must be 0 (cp.async) or 1 (TMA), got %d", mode);
   return kp::g_f1_tma_staging.exchange(mode);
+}
+
+int kp_set_operand_repack(int mode) {
+  if (mode < 0 || mode > 2)
+    return fail(KP_EINVAL, "repack mode must be 0 (never), 1 (when it pays) or 2 (always), got %d", mode);
+  return g_operand_repack.exchange(mode);
 }
 
 int kp_gemm_plan(int id, int m, int k, int n, int batch, int num_sms, int* k_slices, int* k_per_slice) {

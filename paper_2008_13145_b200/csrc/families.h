@@ -61,6 +61,10 @@ cudaError_t im2col3x3_nhwc_pad_launch(const float* x, int B, int H, int W, int C
 cudaError_t im2col3x3_nhwc_bf16_launch(const float* x, int B, int H, int W, int C, void* out, int kpad,
                                        cudaStream_t s);
 cudaError_t cast_bf16_launch(const float* x, int64_t n, void* out, cudaStream_t s);
+// Copy batch x rows x cols elements (es bytes each; source pitch ld, batch stride sbatch)
+// into rows pitched to ldd (a multiple of 16 bytes), batch stride rows * ldd.
+cudaError_t repack_rows_launch(const void* src, int64_t ld, int64_t sbatch, int rows, int cols, int batch, int es,
+                               void* dst, int64_t ldd, cudaStream_t s);
 
 // FFMA peak probe.
 cudaError_t ffma_peak_launch(float* sink, int blocks, int threads, int iters, bool packed, cudaStream_t s);

@@ -196,6 +196,32 @@ int grid_for(int64_t total, int threads) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+
+// Row repack for operands TMA cannot address (row pitch not a multiple of 16 bytes, e.g.
+// raw k = 27 im2col rows): copies `rows` x `cols` elements of each batch into rows
+// pitched to `ldd` (a multiple of 16 bytes).  One thread per destination 16-byte chunk;
+// the pad elements past `cols` are written as zeros (the tensor maps never read them).
+template <typename T>
+__global__ void repack_rows_kernel(const T* __restrict__ src, int64_t ld, int64_t sbatch, int rows, int cols,
+                                   T* __restrict__ dst, int64_t ldd, int64_t chunks_per_row, int64_t total) {
+  constexpr int V = 16 / sizeof(T);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t rq = i / chunks_per_row;
+    const int q = static_cast<int>(i - rq * chunks_per_row);
+    const int64_t b = rq / rows;
+    const int64_t r = rq - b * rows;
+    const T* in = src + b * sbatch + r * ld;
+    T v[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const int c = q * V + e;
+      v[e] = c < cols ? in[c] : T(0);
+    }
+    *reinterpret_cast<uint4*>(dst + (b * rows + r) * ldd + static_cast<int64_t>(q) * V) =
+        *reinterpret_cast<const uint4*>(v);
+  }
+}
 }  // namespace
 
 cudaError_t im2col3x3_nhwc_launch(const float* x, int B, int H, int W, int C, float* out, int64_t ldo,
@@ -247,6 +273,22 @@ cudaError_t maxpool2_nhwc_launch(const float* x, int B, int H, int W, int C, flo
     return cudaGetLastError();
   }
   maxpool2_nhwc_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, B, H, W, C, out);
+  return cudaGetLastError();
+}
+
+
+cudaError_t repack_rows_launch(const void* src, int64_t ld, int64_t sbatch, int rows, int cols, int batch, int es,
+                               void* dst, int64_t ldd, cudaStream_t s) {
+  if ((es != 2 && es != 4) || !aligned16(dst) || (ldd * es) % 16 != 0 || ldd < cols) return cudaErrorInvalidValue;
+  const int64_t chunks = ldd * es / 16;
+  const int64_t total = static_cast<int64_t>(batch) * rows * chunks;
+  if (total == 0) return cudaSuccess;
+  if (es == 2)
+    repack_rows_kernel<uint16_t><<<grid_for(total, 256), 256, 0, s>>>(
+        static_cast<const uint16_t*>(src), ld, sbatch, rows, cols, static_cast<uint16_t*>(dst), ldd, chunks, total);
+  else
+    repack_rows_kernel<uint32_t><<<grid_for(total, 256), 256, 0, s>>>(
+        static_cast<const uint32_t*>(src), ld, sbatch, rows, cols, static_cast<uint32_t*>(dst), ldd, chunks, total);
   return cudaGetLastError();
 }
 

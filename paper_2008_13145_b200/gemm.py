@@ -267,6 +267,17 @@ def set_simt_staging(mode: str) -> str:
     return "tma" if prev else "cp.async"
 
 
+def set_operand_repack(mode: str) -> str:
+    """Operands whose rows TMA cannot address (kp_set_operand_repack): "auto" repacks them
+    into 16-byte-pitched scratch when that pays (default), "always", or "never" (in-kernel
+    staging); returns the previous mode.  Results are the same either way."""
+    modes = {"never": 0, "auto": 1, "always": 2}
+    if mode not in modes:
+        raise ValueError(f"repack mode must be one of {sorted(modes)}, got {mode!r}")
+    prev = _lib.check(_lib.load().kp_set_operand_repack(modes[mode]), "kp_set_operand_repack")
+    return {v: k for k, v in modes.items()}[prev]
+
+
 def ffma_peak_tflops(packed: bool = False, stream: torch.cuda.Stream | None = None) -> float:
     """Measured FP32 peak of the current device (kp_ffma_peak): scalar FFMA or,
     with ``packed``, sm_100 FFMA2."""

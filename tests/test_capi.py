@@ -171,6 +171,21 @@ def test_simt_staging_switch(lib):
         gemm.set_simt_staging("ldgsts")
 
 
+def test_operand_repack_switch(lib):
+    """kp_set_operand_repack: 1 (repack unaligned rows when it pays, default) / 2 (always)
+    / 0 (never: in-kernel staging); the previous mode is returned."""
+    from paper_2008_13145_b200 import gemm
+    assert gemm.set_operand_repack("always") == "auto"
+    try:
+        assert gemm.set_operand_repack("never") == "always"
+    finally:
+        assert gemm.set_operand_repack("auto") == "never"
+    assert lib.kp_set_operand_repack(3) == _lib.KP_EINVAL
+    assert lib.kp_set_operand_repack(-1) == _lib.KP_EINVAL
+    with pytest.raises(ValueError):
+        gemm.set_operand_repack("sometimes")
+
+
 def test_conv3x3_supported_query(lib):
     """kp_conv3x3_supported needs no GPU: SIMT variants with TMA staging and C a multiple
     of their k-tile depth; never the paper / tensor-core families; bad ids -ENOENT."""

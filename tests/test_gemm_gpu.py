@@ -54,6 +54,26 @@ def test_all_640_configs_bit_exact(cuda_device, family, shape):
     assert not bad, f"{len(bad)} configs differ, e.g. {bad[:5]}"
 
 
+@pytest.mark.parametrize("mode", ["always", "never"])
+@pytest.mark.parametrize("shape", [(37, 27, 61, 3), (33, 147, 70, 2), (32, 1231, 27, 1)])
+def test_simt_unaligned_rows_both_staging_paths(cuda_device, shape, mode):
+    """Unaligned rows (k = 27 / 147 / 1231, n = 61 / 70 / 27 unpitched), repacked into
+    16-byte-pitched scratch for the TMA path ("always") or staged in-kernel with 4-byte
+    cp.async copies ("never"): bit-identical to the oracle either way."""
+    A, B = _pair(*shape)
+    dA, dB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    cache, bad = {}, []
+    prev = gemm.set_operand_repack(mode)
+    try:
+        for cfg in CONFIGS[::3]:
+            got = gemm.matmul(dA, dB, cfg, "simt").cpu().numpy()
+            if not np.array_equal(_bits(got), _want(A, B, cfg, "simt", cache)):
+                bad.append(cfg.as_tuple())
+    finally:
+        gemm.set_operand_repack(prev)
+    assert not bad, f"{len(bad)} configs differ, e.g. {bad[:5]}"
+
+
 @pytest.mark.parametrize("shape", [(64, 128, 96, 1), (33, 147, 70, 2)])
 def test_all_640_configs_single_chain_when_unsliced(cuda_device, shape):
     """With k-slicing capped at 1 every SIMT config is the paper's single fp32 chain."""

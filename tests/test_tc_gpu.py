@@ -69,11 +69,18 @@ def test_ragged_and_batched(cuda_device, fam, m, k, n, batch):
 
 @pytest.mark.parametrize("fam", ["bf16", "tf32"])
 @pytest.mark.parametrize("m,k,n,batch", [(64, 27, 64, 1), (1000, 147, 64, 1), (77, 33, 45, 2), (5, 1, 3, 1)])
-def test_unaligned_rows_use_lsu_staging(cuda_device, fam, m, k, n, batch):
-    """Rows that TMA cannot address (k*elem or n*elem not a multiple of 16 B) run through
-    the LSU staging path with the same tolerance (grid totality, dataset.py:259-264)."""
-    for cfg in gemm.family_configs(fam)[::2]:
-        _check(fam, cfg, m, k, n, batch, cuda_device, bcast=(batch > 1), seed=k)
+@pytest.mark.parametrize("repack", ["always", "never", "auto"])
+def test_unaligned_rows(cuda_device, fam, m, k, n, batch, repack):
+    """Rows that TMA cannot address (k*elem or n*elem not a multiple of 16 B): copied into
+    16-byte-pitched scratch for the TMA path, or staged in-kernel by the LSU loaders
+    (kp_set_operand_repack); same tolerance either way (grid totality,
+    dataset.py:259-264)."""
+    prev = gemm.set_operand_repack(repack)
+    try:
+        for cfg in gemm.family_configs(fam)[::2]:
+            _check(fam, cfg, m, k, n, batch, cuda_device, bcast=(batch > 1), seed=k)
+    finally:
+        gemm.set_operand_repack(prev)
 
 
 @pytest.mark.parametrize("fam", ["bf16", "tf32"])
