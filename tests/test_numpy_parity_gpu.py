@@ -63,6 +63,27 @@ def test_vgg16_b16_layer_shapes_match_numpy(cuda_device):
         del dA, dB
 
 
+def test_paper_sample_problems_match_numpy(cuda_device):
+    """The paper's three sample problems (shapes.PAPER_SAMPLES)
+    -- batched m=512 k=784 n=512 x16, rectangular 512x4608x784 and the long accumulation
+    32x12321x27 (unaligned rows) -- on the row-best SIMT config of the measured table and
+    the C1 config, against np.matmul fp32 per batch."""
+    from paper_2008_13145_b200.dataset import parse_benchmark_csv
+    import bench
+
+    pm = parse_benchmark_csv(bench.DEFAULT_TABLE.read_text())
+    rng = np.random.default_rng(284)
+    for p in shapes.PAPER_SAMPLES:
+        best = pm.configs[int(pm.values[list(pm.problems).index(p)].argmax())]
+        A = rng.uniform(-1, 1, (p.batch, p.m, p.k)).astype(np.float32)
+        B = rng.uniform(-1, 1, (p.batch, p.k, p.n)).astype(np.float32)
+        dA, dB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+        for cfg in (best, C1):
+            C = gemm.matmul(dA, dB, cfg, "simt").cpu().numpy()
+            for b in range(p.batch):
+                _compare(C[b], A[b], B[b], p.k, f"{p} simt{cfg.as_tuple()} batch {b}")
+
+
 def test_out_must_not_be_overrun_or_foreign(cuda_device):
     dev = cuda_device
     A = torch.rand(3, 8, 5, device=dev)
