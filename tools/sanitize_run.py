@@ -2,7 +2,9 @@
 synccheck): F0 and F1 vector + scalar (unaligned) paths, tcgen05 TMA and LSU paths,
 k-sliced cluster launches (F1 and tcgen05: DSMEM slice reduction), the tcgen05
 partial-last-wave split, the TMA-store epilogue, epilogue bias/ReLU, kp_bench_sets,
-im2col (plain, padded, bf16), the bf16 cast and max-pool."""
+im2col (plain, padded, bf16), the bf16 cast and max-pool; round 2: unaligned-row repack
+and in-kernel staging (both modes), 16-CTA k-slice clusters, tcgen05 CTA pairs and the
+TMA-im2col implicit-GEMM convolution."""
 import sys
 
 import torch
@@ -65,5 +67,27 @@ cols = torch.empty(2 * 36, 45, device=dev)
 _lib.check(lib.kp_im2col3x3_nhwc(x.data_ptr(), 2, 6, 6, 5, cols.data_ptr(), 45, None), "im2col")
 y = torch.empty(2, 3, 3, 5, device=dev)
 _lib.check(lib.kp_maxpool2x2_nhwc(x.data_ptr(), 2, 6, 6, 5, y.data_ptr(), None), "pool")
+# round 2: unaligned rows through the repack pass and through in-kernel staging
+for mode in ("always", "never"):
+    prev = gemm.set_operand_repack(mode)
+    for fam, cfg in (("simt", KernelConfig(8, 4, 4, 8, 8)), ("bf16", gemm.family_configs("bf16")[0]),
+                     ("tf32", gemm.family_configs("tf32")[1])):
+        dt = gemm.input_dtype(fam)
+        gemm.matmul(torch.rand(300, 27, device=dev).to(dt), torch.rand(27, 61, device=dev).to(dt), cfg, fam)
+    gemm.set_operand_repack(prev)
+# a 16-CTA (non-portable) k-slice cluster: a grid under 0.15 tiles per SM
+cfg16 = KernelConfig(8, 4, 2, 1, 64)
+p16 = ProblemSize(8, 4096, 1000, 1)
+assert gemm.k_slice_plan(cfg16, p16)[0] > 8, gemm.k_slice_plan(cfg16, p16)
+gemm.matmul(torch.rand(8, 4096, device=dev), torch.rand(4096, 1000, device=dev), cfg16, "simt")
+# tcgen05 CTA pairs (256-row tiles), both families
+for fam in ("bf16", "tf32"):
+    pair = next(c for c in gemm.family_configs(fam) if c.tile_rows == 256)
+    dt = gemm.input_dtype(fam)
+    gemm.matmul(torch.rand(600, 256, device=dev).to(dt), torch.rand(256, 520, device=dev).to(dt), pair, fam)
+# implicit-GEMM 3x3 convolution (TMA im2col copies)
+xc = torch.rand(2, 8, 8, 64, device=dev)
+wc = torch.rand(9 * 64, 64, device=dev)
+gemm.conv3x3(xc, wc, gemm.variant_id(KernelConfig(8, 8, 8, 16, 8), "simt"))
 torch.cuda.synchronize()
 print("sanitize run ok")
