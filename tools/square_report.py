@@ -14,7 +14,8 @@ for fam, name in (("paper", "square_paper"), ("simt", "square_simt"), ("tf32", "
     pm = dataset.parse_benchmark_csv((ROOT / "data" / "sweeps" / f"{name}.csv").read_text())
     fams[fam] = {(p.m, p.k, p.n): (float(pm.values[i].max()), pm.configs[int(pm.values[i].argmax())].as_tuple())
                  for i, p in enumerate(pm.problems)}
-cub = json.loads((ROOT / "profiles" / "raw" / "r1_square_cublas.json").read_text())
+cub_path = Path(sys.argv[1]) if len(sys.argv) > 1 else ROOT / "profiles" / "raw" / "r1_square_cublas.json"
+cub = json.loads(cub_path.read_text())
 print("| m,k,n | paper F0 best | simt F1 best | tf32 best | bf16 best | cuBLAS fp32 | cuBLAS tf32 | cuBLAS bf16 |")
 print("|---|---|---|---|---|---|---|---|")
 for key, row in cub.items():
@@ -25,5 +26,6 @@ for key, row in cub.items():
         cells.append(f"{v[0] / 1e3:.1f} `{v[1]}`" if v else "-")
     print(f"| {m},{k},{n} | " + " | ".join(cells) + " | " +
           " | ".join(f"{row[c] / 1e3:.1f}" for c in ("cublas_fp32", "cublas_tf32", "cublas_bf16")) + " |")
-print("\nTFLOP/s; best config per family from data/sweeps (CUDA-event sweep, warm L2); cuBLAS via torch.matmul "
-      "(comparison only).")
+print("\nTFLOP/s; best config per family from data/sweeps (sweep protocol: median of 3 CUDA-event loops of "
+      ">= 20 ms, operands rotated over 2 x L2 for small problems); cuBLAS via torch.matmul, one >= 20 ms loop "
+      "after 2 warm-ups (comparison only; shorter sustained load, so less power-capping on the largest GEMMs).")
