@@ -307,3 +307,23 @@ def test_bench_sets_rotation_and_median(cuda_device):
         assert torch.allclose(o.C[0], o.A[0] @ o.B[0], rtol=1e-5, atol=1e-5)
     with pytest.raises(ValueError):
         gemm.bench_sets(vid, sets, repeats=0)
+
+
+@pytest.mark.parametrize("shape,cfg", [((8, 4096, 1000, 1), (8, 4, 2, 1, 64)), ((16, 4096, 1000, 1), (8, 8, 8, 16, 8)),
+                                       ((4, 4096, 1000, 1), (4, 4, 2, 1, 64))])
+def test_sixteen_cta_slices_bit_exact_repeated(cuda_device, shape, cfg):
+    """Grids under 0.15 tiles per SM run 16-CTA (non-portable) k-slice clusters; repeated
+    launches stay bit-exact against the oracle's slice-ordered sum for the launch plan
+    (profiles/sanitizer/r2/README.md)."""
+    m, k, n, _ = shape
+    config = KernelConfig(*cfg)
+    s, kps = gemm.k_slice_plan(config, dataset_problem((m, k, n, 1)))
+    assert s == 16, (s, kps)
+    A, B = _pair(m, k, n, 1)
+    want = _bits(go.gemm_sliced(A, B, kps))
+    dA, dB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    out = torch.empty(1, m, n, device=cuda_device)
+    for it in range(40):
+        gemm.matmul(dA, dB, config, "simt", out=out)
+        if it % 10 == 9:
+            assert np.array_equal(_bits(out.cpu().numpy()), want), f"launch {it} differs"
