@@ -302,6 +302,20 @@ def run_reference(args, world, rank):
     return 0
 
 
+def c_dispatch_cost(disp, problems, reps: int = 2000) -> float:
+    """Host cost of one runtime selection through the C table (kp_dispatch_select: log2
+    features + tree walk + class -> variant), microseconds per call including the ctypes
+    call; the Dispatcher caches the result per shape, so the timed GEMM loop never pays it."""
+    from paper_2008_13145_b200 import _lib
+
+    lib = _lib.load()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        for p in problems:
+            lib.kp_dispatch_select(disp.handle, p.m, p.k, p.n, p.batch)
+    return (time.perf_counter() - t0) / (reps * len(problems)) * 1e6
+
+
 # ----------------------------------------------------------------- roofline --
 def measured_peaks() -> dict:
     path = ROOT / "MEASURED_PEAKS.json"
@@ -469,6 +483,7 @@ def run_ours(args, world, rank, local):
 
     layers = vgg16_layers(args.batch)
     in_dtype = gemm.input_dtype(args.family)  # fp32, or bf16 operands for the BF16 family
+    sel_t["c_tree_walk_us_per_call"] = c_dispatch_cost(disp, [p for _, p in layers])
     gen = torch.Generator(device=device).manual_seed(1234 + rank)
     bufs = []
     al = 16 // in_dtype.itemsize  # rows pitched to 16 bytes, as the sweep times them (conv1_1: k = 27)
