@@ -228,8 +228,10 @@ int kp_cast_bf16(const float* x, int64_t n, void* out, void* stream);
  * straight from x by TMA im2col copies -- no im2col buffer in HBM.  Same launch plan
  * (k-slices) and fp32 chain as the explicit path, so the output is bit-identical.
  * kp_conv3x3_supported(id, C, Cout) returns 1 when variant id can run it (SIMT variant
- * with TMA staging, i.e. CTA tile <= 256 columns, C a multiple of its k-tile depth,
- * Cout % 4 == 0), 0 when not, < 0 for a bad id.  x, w and out must be 16-byte aligned. */
+ * with TMA staging, i.e. CTA tile <= 256 columns, C a multiple of its k-tile depth; or a
+ * TF32 variant with C % 32 == 0 -- its TMA producer loads 128-byte-swizzled im2col boxes
+ * into the tcgen05 ring, 1-CTA kernel; Cout % 4 == 0 for both), 0 when not (PAPER, BF16),
+ * < 0 for a bad id.  x, w and out must be 16-byte aligned. */
 int kp_conv3x3_supported(int id, int C, int Cout);
 int kp_conv3x3_nhwc_ex(int id, const float* x, int B, int H, int W, int C, const float* w, int Cout, float* out,
                        const float* bias, int flags, void* stream);

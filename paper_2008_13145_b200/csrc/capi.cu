@@ -373,7 +373,8 @@ int launch(int id, const kp::GemmArgs& p0, cudaStream_t s) {
       Repacked rp;
       const bool simt_tma = v.family == KP_FAMILY_SIMT && reg.f1[v.index].tma_ok && p.conv_c == 0 &&
                             kp::g_f1_tma_staging.load(std::memory_order_relaxed) != 0;
-      if ((simt_tma || v.family != KP_FAMILY_SIMT) && g_operand_repack.load(std::memory_order_relaxed) != 0) {
+      if ((simt_tma || (v.family != KP_FAMILY_SIMT && p.conv_c == 0)) &&
+          g_operand_repack.load(std::memory_order_relaxed) != 0) {
         const bool tc = v.family != KP_FAMILY_SIMT;
         const int bk = tc ? kp::tc_tile_k(v.family) : reg.f1[v.index].bk;
         e = repack_unaligned(p, v.family == KP_FAMILY_BF16 ? 2 : 4, tc, bk,
@@ -497,7 +498,10 @@ int kp_conv3x3_supported(int id, int C, int Cout) {
   Registry& reg = registry();
   if (id < 0 || id >= static_cast<int>(reg.variants.size())) return fail(KP_ENOENT, "unknown variant id %d", id);
   const Variant& v = reg.variants[id];
-  if (v.family != KP_FAMILY_SIMT || C < 1 || Cout < 1) return 0;
+  if (C < 1 || Cout < 1) return 0;
+  // TF32 (fp32 activations): im2col boxes of 32 channels = one 128-byte K slab
+  if (v.family == KP_FAMILY_TF32) return (C % kp::tc_tile_k(v.family) == 0 && Cout % 4 == 0) ? 1 : 0;
+  if (v.family != KP_FAMILY_SIMT) return 0;  // PAPER: the paper's kernel; BF16: bf16 operands only
   const kp::F1Entry& e = reg.f1[v.index];
   return (e.tma_ok && C % e.bk == 0 && Cout % 4 == 0) ? 1 : 0;
 }

@@ -77,6 +77,19 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// TMA im2col load (implicit-GEMM 3x3 convolution): BM consecutive output pixels (w fastest,
+// then h, then image) from base pixel (w, h, n) of the map's bounding box, each contributing
+// the map's channelsPerPixel channels from c of input pixel (w + dx, h + dy); zero outside
+// the image.  The rows land 128B-swizzled exactly as the tiled A box would.
+__device__ __forceinline__ void tma_im2col_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c, int w, int h,
+                                              int n, uint16_t dx, uint16_t dy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(dx), "h"(dy)
+      : "memory");
+}
+
 // TMA store of a 32 x 32 fp32 box (128B-swizzled smem) to C at (x = col, y = row, z = batch).
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y, int z) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
@@ -353,7 +366,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* sa = smem + s * Cfg::STAGE_BYTES;
         uint8_t* sb = sa + Cfg::A_BYTES;
         mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
-        tma_load_3d(sa, &mapA, &full[s], (kt0 + kt) * Cfg::BK, m0, za);
+        if (p.conv_c > 0) {
+          // implicit conv: k-tile (kt0 + kt) lies inside one filter tap (conv_c % BK == 0)
+          const int k0 = (kt0 + kt) * Cfg::BK, tap = k0 / p.conv_c, c0 = k0 - tap * p.conv_c;
+          const int tr = m0 / p.conv_w, w = m0 - tr * p.conv_w, img = tr / p.conv_h, h = tr - img * p.conv_h;
+          tma_im2col_4d(sa, &mapA, &full[s], c0, w - 1, h - 1, img, static_cast<uint16_t>(tap % 3),
+                        static_cast<uint16_t>(tap / 3));
+        } else {
+          tma_load_3d(sa, &mapA, &full[s], (kt0 + kt) * Cfg::BK, m0, za);
+        }
 #pragma unroll
         for (int j = 0; j < BN / Cfg::NATOM; ++j)
           tma_load_3d(sb + j * (Cfg::BK * 128), &mapB, &full[s], n0 + j * Cfg::NATOM, (kt0 + kt) * Cfg::BK, zb);
@@ -766,6 +787,23 @@ using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, voi
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(ptr);
+  }
+  return fn;
+}
+
 EncodeFn encode_fn() {
   static EncodeFn fn = nullptr;
   if (!fn) {
@@ -932,10 +970,28 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
       if (!a_batched) strides[1] = (strides[1] + 15) / 16 * 16;
       cuuint32_t box[3] = {static_cast<cuuint32_t>(Cfg::BK), static_cast<cuuint32_t>(BM), 1};
       cuuint32_t es[3] = {1, 1, 1};
-      if (enc(&ma, dt, 3, const_cast<void*>(p.A), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      if (p.conv_c > 0) {
+        // implicit conv: A is the NHWC activation; im2col boxes of BK channels x BM pixels,
+        // bounding box corners -1 / -1 (base pixel = output pixel - 1 in w and h)
+        EncodeIm2colFn enc2 = encode_im2col_fn();
+        const int imgs = p.m / (p.conv_h * p.conv_w);
+        cuuint64_t idims[4] = {static_cast<cuuint64_t>(p.conv_c), static_cast<cuuint64_t>(p.conv_w),
+                               static_cast<cuuint64_t>(p.conv_h), static_cast<cuuint64_t>(imgs)};
+        cuuint64_t istrides[3] = {static_cast<cuuint64_t>(p.conv_c) * Cfg::ES,
+                                  static_cast<cuuint64_t>(p.conv_w) * p.conv_c * Cfg::ES,
+                                  static_cast<cuuint64_t>(p.conv_h) * p.conv_w * p.conv_c * Cfg::ES};
+        const int lower[2] = {-1, -1}, upper[2] = {-1, -1};
+        cuuint32_t ies[4] = {1, 1, 1, 1};
+        if (!enc2 || enc2(&ma, dt, 4, const_cast<void*>(p.A), idims, istrides, lower, upper,
+                          static_cast<cuuint32_t>(Cfg::BK), static_cast<cuuint32_t>(BM), ies,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          return cudaErrorInvalidValue;
+      } else if (enc(&ma, dt, 3, const_cast<void*>(p.A), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
         return cudaErrorInvalidValue;
+      }
     }
     {
       cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.n), static_cast<cuuint64_t>(p.k),
@@ -953,7 +1009,7 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   }
   if constexpr (PAIR_STAGES > 0) {
     // CTA pairs for persistent TMA launches (no tail split: the pair kernel runs every tile)
-    if (!lsu && p.kslices <= 1)
+    if (!lsu && p.kslices <= 1 && p.conv_c == 0)
       return launch_pair<kTF32, BN, PAIR_STAGES>(p, ma, mb, mc, a_batched, b_batched, tma_store, s);
     tail = 0;
   }

@@ -181,7 +181,7 @@ def conv3x3(x: torch.Tensor, w: torch.Tensor, vid: int, bias: torch.Tensor | Non
             out: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
     """3x3 / stride 1 / pad 1 convolution of NHWC ``x`` (B, H, W, Cin) fp32 with the
     (9*Cin, Cout) weight matrix ``w`` (k order (dy, dx, c), as kp_im2col3x3_nhwc) as an
-    implicit GEMM on SIMT variant ``vid`` (TMA im2col copies; kp_conv3x3_nhwc_ex).  The
+    implicit GEMM on SIMT or TF32 variant ``vid`` (TMA im2col copies; kp_conv3x3_nhwc_ex).  The
     result, (B, H, W, Cout), is bit-identical to im2col + matmul with the same variant."""
     if x.dim() != 4 or not x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous():
         raise ValueError("x must be a contiguous (B, H, W, C) fp32 CUDA tensor")

@@ -188,7 +188,8 @@ def test_operand_repack_switch(lib):
 
 def test_conv3x3_supported_query(lib):
     """kp_conv3x3_supported needs no GPU: SIMT variants with TMA staging and C a multiple
-    of their k-tile depth; never the paper / tensor-core families; bad ids -ENOENT."""
+    of their k-tile depth, TF32 variants with C % 32 == 0; never the paper or BF16
+    families; bad ids -ENOENT."""
     from paper_2008_13145_b200 import gemm
     vid = gemm.variant_id(KernelConfig(8, 8, 8, 16, 8), "simt")
     assert lib.kp_conv3x3_supported(vid, 64, 64) == 1
@@ -197,3 +198,10 @@ def test_conv3x3_supported_query(lib):
     assert lib.kp_conv3x3_supported(gemm.variant_id(KernelConfig(8, 8, 8, 1, 128), "simt"), 64, 64) == 0  # BN 1024
     assert lib.kp_conv3x3_supported(gemm.variant_id(KernelConfig(8, 8, 8, 16, 8), "paper"), 64, 64) == 0
     assert lib.kp_conv3x3_supported(10 ** 6, 64, 64) == _lib.KP_ENOENT
+    for cfg in gemm.family_configs("tf32"):
+        tid = gemm.variant_id(cfg, "tf32")
+        assert lib.kp_conv3x3_supported(tid, 64, 64) == 1
+        assert lib.kp_conv3x3_supported(tid, 48, 64) == 0  # not a whole 32-channel slab
+        assert lib.kp_conv3x3_supported(tid, 64, 62) == 0
+    for cfg in gemm.family_configs("bf16"):
+        assert lib.kp_conv3x3_supported(gemm.variant_id(cfg, "bf16"), 64, 64) == 0

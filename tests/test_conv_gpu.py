@@ -76,3 +76,33 @@ def test_implicit_conv_large_layer_matches_explicit(cuda_device):
         got = gemm.conv3x3(x, w, vid).reshape(-1, 256)
         want = gemm.matmul(cols, w, cfg, "simt")
         assert torch.equal(got.view(torch.int32), want.view(torch.int32)), cfg
+
+
+@pytest.mark.parametrize("B,H,W,C,cout", [(2, 9, 7, 32, 64), (1, 14, 14, 64, 128), (3, 28, 28, 256, 96),
+                                         (16, 14, 14, 512, 512)])
+def test_tf32_implicit_conv_equals_explicit(cuda_device, B, H, W, C, cout):
+    """TF32 family: the tcgen05 producer loads 128-byte-swizzled TMA im2col boxes of 32
+    channels x 128 pixels instead of the tiled A box -- the same operand tiles in shared
+    memory, the same MMA sequence and k-slice plan, so the output equals im2col + the same
+    TF32 variant bit for bit (fused bias + ReLU), and stays within the TF32 bound of the
+    float64 product."""
+    g = torch.Generator(device=cuda_device).manual_seed(B * 7 + C)
+    x = torch.randn(B, H, W, C, device=cuda_device, generator=g)
+    w = torch.randn(9 * C, cout, device=cuda_device, generator=g) * 0.05
+    bias = torch.randn(cout, device=cuda_device, generator=g) * 0.1
+    lib = _lib.load()
+    m, k = B * H * W, 9 * C
+    cols = torch.empty(m, k, device=cuda_device)
+    assert lib.kp_im2col3x3_nhwc(x.data_ptr(), B, H, W, C, cols.data_ptr(), k, None) == 0
+    c64 = cols.double() @ w.double() + bias.double()
+    mag = cols.abs().double() @ w.abs().double() + bias.abs().double()
+    for cfg in gemm.family_configs("tf32"):
+        vid = gemm.variant_id(cfg, "tf32")
+        assert gemm.conv3x3_supported(vid, C, cout)
+        got = gemm.conv3x3(x, w, vid, bias=bias, relu=True).reshape(-1, cout)
+        ref = torch.empty(m, cout, device=cuda_device)
+        assert lib.kp_gemm_ex(vid, m, k, cout, 1, cols.data_ptr(), k, 0, w.data_ptr(), cout, 0, ref.data_ptr(), cout, 0,
+                              bias.data_ptr(), _lib.KP_EPI_RELU, None) == 0
+        assert torch.equal(got.view(torch.int32), ref.view(torch.int32)), (cfg.as_tuple(), gemm.k_slice_plan(vid, ProblemSize(m, k, cout, 1)))
+        err = (got.double() - torch.relu(c64)).abs()
+        assert bool((err <= (2 * 2.0 ** -10 + 2 * k * 2.0 ** -24) * mag + 1e-6).all()), cfg.as_tuple()
