@@ -222,21 +222,28 @@ int kp_im2col3x3_nhwc_pad(const float* x, int B, int H, int W, int C, float* out
  * cast of n elements (n % 8 == 0, 16-byte-aligned pointers). */
 int kp_im2col3x3_nhwc_bf16(const float* x, int B, int H, int W, int C, void* out, int kpad, void* stream);
 int kp_cast_bf16(const float* x, int64_t n, void* out, void* stream);
-/* Implicit-GEMM 3x3 / stride 1 / pad 1 convolution (SIMT family): the GEMM that
- * kp_im2col3x3_nhwc + kp_gemm_ex would run (m = B*H*W, k = 9*C, n = Cout, weights
- * (9*C) x Cout row-major, out (B*H*W) x Cout = NHWC) with the patch rows gathered
- * straight from x by TMA im2col copies -- no im2col buffer in HBM.  Same launch plan
- * (k-slices) and fp32 chain as the explicit path, so the output is bit-identical.
+/* Implicit-GEMM 3x3 / stride 1 / pad 1 convolution: the GEMM that kp_im2col3x3_nhwc
+ * (or kp_im2col3x3_nhwc_bf16) + kp_gemm_ex would run (m = B*H*W, k = 9*C, n = Cout,
+ * weights (9*C) x Cout row-major, out (B*H*W) x Cout = NHWC fp32) with the patch rows
+ * gathered straight from x by TMA im2col copies -- no im2col buffer in HBM.  Same launch
+ * plan (k-slices) and accumulation order as the explicit path, so the output is
+ * bit-identical.  Element types follow kp_gemm: x and w are fp32 for SIMT/TF32 variants
+ * and bf16 for BF16 variants (out is fp32 for all).
  * kp_conv3x3_supported(id, C, Cout) returns 1 when variant id can run it (SIMT variant
- * with TMA staging, i.e. CTA tile <= 256 columns, C a multiple of its k-tile depth; or a
- * TF32 variant with C % 32 == 0 -- its TMA producer loads 128-byte-swizzled im2col boxes
- * into the tcgen05 ring, 1-CTA kernel; Cout % 4 == 0 for both), 0 when not (PAPER, BF16),
- * < 0 for a bad id.  x, w and out must be 16-byte aligned. */
+ * with TMA staging, i.e. CTA tile <= 256 columns, C a multiple of its k-tile depth,
+ * Cout % 4 == 0; a TF32 variant with C % 32 == 0 and Cout % 4 == 0; a BF16 variant with
+ * C % 64 == 0 and Cout % 8 == 0 -- the tensor-core producers load 128-byte-swizzled
+ * im2col boxes into the tcgen05 ring, 1-CTA kernel), 0 when not (PAPER), < 0 for a bad
+ * id.  x, w and out must be 16-byte aligned. */
 int kp_conv3x3_supported(int id, int C, int Cout);
-int kp_conv3x3_nhwc_ex(int id, const float* x, int B, int H, int W, int C, const float* w, int Cout, float* out,
+int kp_conv3x3_nhwc_ex(int id, const void* x, int B, int H, int W, int C, const void* w, int Cout, float* out,
                        const float* bias, int flags, void* stream);
 /* 2x2 / stride 2 max pooling, NHWC: (B, H, W, C) -> (B, H/2, W/2, C). */
 int kp_maxpool2x2_nhwc(const float* x, int B, int H, int W, int C, float* out, void* stream);
+/* The same pooling with a bf16 result (round to nearest even; C % 4 == 0, x 16-byte and
+ * out 8-byte aligned): the BF16 family's implicit-conv operand.  Rounding is monotonic,
+ * so this equals pooling in fp32 and rounding in kp_im2col3x3_nhwc_bf16. */
+int kp_maxpool2x2_nhwc_bf16(const float* x, int B, int H, int W, int C, void* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -86,6 +86,7 @@ SIGNATURES = {
     "kp_gemm_auto_ex": (_i, [_i] + _GEMM_ARGS + [_vp, _i, _vp, _ip]),
     "kp_im2col3x3_nhwc": (_i, [_vp, _i, _i, _i, _i, _vp, _i64, _vp]),
     "kp_maxpool2x2_nhwc": (_i, [_vp, _i, _i, _i, _i, _vp, _vp]),
+    "kp_maxpool2x2_nhwc_bf16": (_i, [_vp, _i, _i, _i, _i, _vp, _vp]),
     "kp_conv3x3_supported": (_i, [_i, _i, _i]),
     "kp_conv3x3_nhwc_ex": (_i, [_i, _vp, _i, _i, _i, _i, _vp, _i, _vp, _vp, _i, _vp]),
     "kp_im2col3x3_nhwc_pad": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _vp]),

@@ -501,12 +501,15 @@ int kp_conv3x3_supported(int id, int C, int Cout) {
   if (C < 1 || Cout < 1) return 0;
   // TF32 (fp32 activations): im2col boxes of 32 channels = one 128-byte K slab
   if (v.family == KP_FAMILY_TF32) return (C % kp::tc_tile_k(v.family) == 0 && Cout % 4 == 0) ? 1 : 0;
-  if (v.family != KP_FAMILY_SIMT) return 0;  // PAPER: the paper's kernel; BF16: bf16 operands only
+  // BF16 (bf16 activations and weights): 64 channels = one 128-byte K slab; weight rows of
+  // Cout bf16 must be 16-byte pitched for the B tensor map
+  if (v.family == KP_FAMILY_BF16) return (C % kp::tc_tile_k(v.family) == 0 && Cout % 8 == 0) ? 1 : 0;
+  if (v.family != KP_FAMILY_SIMT) return 0;  // PAPER: the paper's kernel
   const kp::F1Entry& e = reg.f1[v.index];
   return (e.tma_ok && C % e.bk == 0 && Cout % 4 == 0) ? 1 : 0;
 }
 
-int kp_conv3x3_nhwc_ex(int id, const float* x, int B, int H, int W, int C, const float* w, int Cout, float* out,
+int kp_conv3x3_nhwc_ex(int id, const void* x, int B, int H, int W, int C, const void* w, int Cout, float* out,
                        const float* bias, int flags, void* stream) {
   if (B < 1 || H < 1 || W < 1 || C < 1 || Cout < 1) return fail(KP_EINVAL, "conv dims must be >= 1");
   if (static_cast<int64_t>(B) * H * W > 0x7fffffffLL || 9LL * C > 0x7fffffffLL)
@@ -709,6 +712,13 @@ int kp_maxpool2x2_nhwc(const float* x, int B, int H, int W, int C, float* out, v
   if (B < 1 || H < 2 || W < 2 || C < 1) return fail(KP_EINVAL, "bad activation shape");
   cudaError_t e = kp::maxpool2_nhwc_launch(x, B, H, W, C, out, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? KP_OK : cuda_fail(e, "maxpool launch");
+}
+
+int kp_maxpool2x2_nhwc_bf16(const float* x, int B, int H, int W, int C, void* out, void* stream) {
+  if (!x || !out) return fail(KP_EINVAL, "null pointer");
+  if (B < 1 || H < 2 || W < 2 || C < 1 || C % 4 != 0) return fail(KP_EINVAL, "bad activation shape (C % 4 == 0)");
+  cudaError_t e = kp::maxpool2_nhwc_bf16_launch(x, B, H, W, C, out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? KP_OK : cuda_fail(e, "maxpool (bf16 out) launch (x 16-byte, out 8-byte aligned)");
 }
 
 int kp_dispatch_load(int n_nodes, const int32_t* feature, const double* threshold, const int32_t* left,

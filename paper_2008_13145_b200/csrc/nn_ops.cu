@@ -166,6 +166,27 @@ __global__ void maxpool2_nhwc_vec4_kernel(const float4* __restrict__ x, int B, i
   }
 }
 
+// 2x2 / stride 2 max pool of fp32 NHWC activations written as bf16 (round to nearest even):
+// the BF16 family's implicit-conv operand.  rn() is monotonic, so rn(max) == max(rn) and
+// this equals pooling first and rounding in the next layer's bf16 im2col (C % 4 == 0).
+__global__ void maxpool2_nhwc_bf16_kernel(const float4* __restrict__ x, int B, int H, int W, int C4,
+                                          uint2* __restrict__ out, unsigned total) {
+  const unsigned Ho = H / 2, Wo = W / 2;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned c4 = i % C4;
+    unsigned r = i / C4;
+    const unsigned wo = r % Wo;
+    r /= Wo;
+    const unsigned ho = r % Ho;
+    const unsigned b = r / Ho;
+    const float4* base = x + ((static_cast<int64_t>(b) * H + 2 * ho) * W + 2 * wo) * C4 + c4;
+    const float4 a0 = __ldg(base), a1 = __ldg(base + C4);
+    const float4 a2 = __ldg(base + static_cast<int64_t>(W) * C4), a3 = __ldg(base + static_cast<int64_t>(W) * C4 + C4);
+    out[i] = make_uint2(pack_bf16x2(fmaxf(fmaxf(a0.x, a1.x), fmaxf(a2.x, a3.x)), fmaxf(fmaxf(a0.y, a1.y), fmaxf(a2.y, a3.y))),
+                        pack_bf16x2(fmaxf(fmaxf(a0.z, a1.z), fmaxf(a2.z, a3.z)), fmaxf(fmaxf(a0.w, a1.w), fmaxf(a2.w, a3.w))));
+  }
+}
+
 // 2x2 / stride 2 max pool; one thread per output element (channel fastest).
 __global__ void maxpool2_nhwc_kernel(const float* __restrict__ x, int B, int H, int W, int C, float* __restrict__ out) {
   const int Ho = H / 2, Wo = W / 2;
@@ -273,6 +294,17 @@ cudaError_t maxpool2_nhwc_launch(const float* x, int B, int H, int W, int C, flo
     return cudaGetLastError();
   }
   maxpool2_nhwc_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, B, H, W, C, out);
+  return cudaGetLastError();
+}
+
+cudaError_t maxpool2_nhwc_bf16_launch(const float* x, int B, int H, int W, int C, void* out, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(B) * (H / 2) * (W / 2) * C;
+  if (C % 4 != 0 || !aligned16(x) || (reinterpret_cast<uintptr_t>(out) % 8) != 0 || total / 4 >= 0x7fffffffLL)
+    return cudaErrorInvalidValue;
+  const unsigned t4 = static_cast<unsigned>(total / 4);
+  if (t4 == 0) return cudaSuccess;
+  maxpool2_nhwc_bf16_kernel<<<grid_for(t4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(x), B, H, W, C / 4,
+                                                                reinterpret_cast<uint2*>(out), t4);
   return cudaGetLastError();
 }
 

@@ -179,16 +179,18 @@ def conv3x3_supported(vid: int, cin: int, cout: int) -> bool:
 
 def conv3x3(x: torch.Tensor, w: torch.Tensor, vid: int, bias: torch.Tensor | None = None, relu: bool = False,
             out: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
-    """3x3 / stride 1 / pad 1 convolution of NHWC ``x`` (B, H, W, Cin) fp32 with the
-    (9*Cin, Cout) weight matrix ``w`` (k order (dy, dx, c), as kp_im2col3x3_nhwc) as an
-    implicit GEMM on SIMT or TF32 variant ``vid`` (TMA im2col copies; kp_conv3x3_nhwc_ex).  The
-    result, (B, H, W, Cout), is bit-identical to im2col + matmul with the same variant."""
-    if x.dim() != 4 or not x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous():
-        raise ValueError("x must be a contiguous (B, H, W, C) fp32 CUDA tensor")
+    """3x3 / stride 1 / pad 1 convolution of NHWC ``x`` (B, H, W, Cin) with the (9*Cin, Cout)
+    weight matrix ``w`` (k order (dy, dx, c), as kp_im2col3x3_nhwc) as an implicit GEMM on
+    SIMT, TF32 or BF16 variant ``vid`` (TMA im2col copies; kp_conv3x3_nhwc_ex).  ``x`` and
+    ``w`` are fp32 for SIMT/TF32 variants and bf16 for BF16 variants; the fp32 result,
+    (B, H, W, Cout), is bit-identical to im2col + matmul with the same variant."""
+    dt = input_dtype(variant_info(vid)[1])
+    if x.dim() != 4 or not x.is_cuda or x.dtype != dt or not x.is_contiguous():
+        raise ValueError(f"x must be a contiguous (B, H, W, C) {dt} CUDA tensor for variant {vid}")
     B, H, W, C = x.shape
-    if w.shape[0] != 9 * C or w.dim() != 2 or w.dtype != torch.float32 or not w.is_contiguous() \
+    if w.shape[0] != 9 * C or w.dim() != 2 or w.dtype != dt or not w.is_contiguous() \
             or w.device != x.device:
-        raise ValueError(f"w must be a contiguous ({9 * C}, Cout) fp32 tensor on {x.device}")
+        raise ValueError(f"w must be a contiguous ({9 * C}, Cout) {dt} tensor on {x.device}")
     cout = w.shape[1]
     if out is None:
         out = torch.empty(B, H, W, cout, device=x.device)

@@ -8,6 +8,13 @@ is ``kp_maxpool2x2_nhwc``; fc6/fc7/fc8 are GEMMs with m = B.  Activations are NH
 fp32, so each GEMM output is directly the next layer's input.  Weights are He-normal
 random (no network access for trained weights), seeded, identical on every rank.
 
+Convolutions whose dispatched variant supports it run as implicit GEMMs instead
+(``kp_conv3x3_nhwc_ex``: TMA im2col copies gather the patches from the activation, no
+im2col buffer).  The BF16 family keeps fp32 activations between layers (the GEMM epilogue
+writes fp32); its implicit convs read a bf16 copy made by ``kp_cast_bf16`` or, after a
+pool, by ``kp_maxpool2x2_nhwc_bf16`` -- the same round-to-nearest of the same fp32 values
+the explicit path's bf16 im2col applies, so both paths give identical logits.
+
 Data parallelism (configs[2] at 1/2/4/8 GPUs): each rank runs its own images with
 replicated weights; there is no collective on the data path.  The whole forward for a
 fixed batch can be captured once in a CUDA graph (``Vgg16.capture``) because all
@@ -53,7 +60,7 @@ class Vgg16:
 
     def __init__(self, dispatcher, batch: int, device, seed: int = 0, weights=None, implicit: bool = True):
         self.disp = dispatcher
-        # implicit: conv layers whose dispatched SIMT variant supports it run as implicit
+        # implicit: conv layers whose dispatched variant supports it run as implicit
         # GEMMs (kp_conv3x3_nhwc_ex, TMA im2col) instead of im2col + GEMM
         self.implicit = implicit
         self.batch = batch
@@ -74,10 +81,28 @@ class Vgg16:
         self.convs = [(w.to(wdt).contiguous(), b) for w, b in self.convs]
         self.fcs = [(w.to(self.device).to(wdt).contiguous(), b.to(self.device).contiguous()) for w, b in fcs]
         B = batch
+        # per conv layer: (B, H, Cin, Cout, m, k as launched, variant, implicit?)
+        self.layers = []
+        H = 224
+        for item in VGG16_PLAN:
+            if item == "M":
+                H //= 2
+                continue
+            cin, cout = item
+            m, k = B * H * H, 9 * cin
+            k_launch = k if k % align == 0 else self.k_pad0
+            vid = self.disp.variant(ProblemSize(m, k, cout, 1))
+            implicit = self.implicit and gemm.conv3x3_supported(vid, cin, cout)
+            self.layers.append((B, H, cin, cout, m, k_launch, vid, implicit))
         # ping-pong activation buffers sized for the largest layer output (B*224*224*64)
         act = B * 224 * 224 * 64
         self.act = [torch.empty(act, device=self.device) for _ in range(2)]
-        self.cols = torch.empty(B * 224 * 224 * 9 * 64, device=self.device, dtype=wdt)  # conv1_2 im2col
+        # im2col rows for the explicit layers only (conv1_1 alone when the rest are implicit)
+        cols = max([m * k for (_, _, _, _, m, k, _, imp) in self.layers if not imp], default=8)
+        self.cols = torch.empty(cols, device=self.device, dtype=wdt)
+        # bf16 copy of an implicit conv's input (BF16 family)
+        self.act16 = (torch.empty(act, device=self.device, dtype=torch.bfloat16)
+                      if self.bf16 and any(lay[-1] for lay in self.layers) else None)
         self.fc_in = torch.empty(B, 7 * 7 * 512, device=self.device, dtype=wdt)  # bf16 fc operands
         self.fc_in2 = torch.empty(B, 4096, device=self.device, dtype=wdt)
         self.input = torch.empty(B, 224, 224, 3, device=self.device)
@@ -110,42 +135,52 @@ class Vgg16:
         lib = _lib.load()
         B, H, C = self.batch, 224, 3
         src = self.input
+        src16 = False  # act16 already holds src rounded to bf16 (a bf16 pool wrote it)
         dst_i = 0
         ci = 0
-        for item in VGG16_PLAN:
+        for pi, item in enumerate(VGG16_PLAN):
             dst = self.act[dst_i]
             if item == "M":
+                nxt = ci if pi + 1 < len(VGG16_PLAN) and VGG16_PLAN[pi + 1] != "M" else None
+                if self.act16 is not None and nxt is not None and nxt < len(self.layers) and self.layers[nxt][-1]:
+                    # the next conv is an implicit BF16 GEMM: pool straight into its bf16 operand
+                    _lib.check(lib.kp_maxpool2x2_nhwc_bf16(src.data_ptr(), B, H, H, C, self.act16.data_ptr(),
+                                                           stream_handle), "kp_maxpool2x2_nhwc_bf16")
+                    src16 = True
+                    H //= 2
+                    continue
                 _lib.check(lib.kp_maxpool2x2_nhwc(src.data_ptr(), B, H, H, C, dst.data_ptr(), stream_handle),
                            "kp_maxpool2x2_nhwc")
                 H //= 2
             else:
-                cin, cout = item
+                _, _, cin, cout, m, k, vid, implicit = self.layers[ci]
                 w, b = self.convs[ci]
                 ci += 1
-                m, k = B * H * H, 9 * cin
-                vid = self.disp.variant(ProblemSize(m, k, cout, 1))
-                if self.implicit and not self.bf16 and gemm.conv3x3_supported(vid, cin, cout):
-                    # implicit GEMM: TMA im2col copies gather the patches from src directly
-                    _lib.check(lib.kp_conv3x3_nhwc_ex(vid, src.data_ptr(), B, H, H, cin, w.data_ptr(), cout,
+                if implicit:
+                    # implicit GEMM: TMA im2col copies gather the patches from the activation
+                    x = src
+                    if self.bf16:
+                        if not src16:
+                            _lib.check(lib.kp_cast_bf16(src.data_ptr(), B * H * H * cin, self.act16.data_ptr(),
+                                                        stream_handle), "kp_cast_bf16")
+                        x = self.act16
+                    _lib.check(lib.kp_conv3x3_nhwc_ex(vid, x.data_ptr(), B, H, H, cin, w.data_ptr(), cout,
                                                       dst.data_ptr(), b.data_ptr(), _lib.KP_EPI_RELU, stream_handle),
                                f"kp_conv3x3_nhwc_ex({B}x{H}x{H}x{cin} -> {cout})")
-                    C = cout
-                    src = dst
-                    dst_i ^= 1
-                    continue
-                if self.bf16:
-                    k = k if k % 8 == 0 else self.k_pad0
+                elif self.bf16:
                     _lib.check(lib.kp_im2col3x3_nhwc_bf16(src.data_ptr(), B, H, H, cin, self.cols.data_ptr(), k,
                                                           stream_handle), "kp_im2col3x3_nhwc_bf16")
-                elif k % 4:  # conv1_1: 16-byte-aligned padded rows
-                    k = self.k_pad0
+                    self._gemm(self.cols, w, b, dst, m, k, cout, True, stream_handle)
+                elif k != 9 * cin:  # conv1_1: 16-byte-aligned padded rows
                     _lib.check(lib.kp_im2col3x3_nhwc_pad(src.data_ptr(), B, H, H, cin, self.cols.data_ptr(), k,
                                                          stream_handle), "kp_im2col3x3_nhwc_pad")
+                    self._gemm(self.cols, w, b, dst, m, k, cout, True, stream_handle)
                 else:
                     _lib.check(lib.kp_im2col3x3_nhwc(src.data_ptr(), B, H, H, cin, self.cols.data_ptr(), k,
                                                      stream_handle), "kp_im2col3x3_nhwc")
-                self._gemm(self.cols, w, b, dst, m, k, cout, True, stream_handle)
+                    self._gemm(self.cols, w, b, dst, m, k, cout, True, stream_handle)
                 C = cout
+                src16 = False
             src = dst
             dst_i ^= 1
         x = src  # (B, 7, 7, 512) NHWC flattened per image = fc6 input rows

@@ -188,8 +188,8 @@ def test_operand_repack_switch(lib):
 
 def test_conv3x3_supported_query(lib):
     """kp_conv3x3_supported needs no GPU: SIMT variants with TMA staging and C a multiple
-    of their k-tile depth, TF32 variants with C % 32 == 0; never the paper or BF16
-    families; bad ids -ENOENT."""
+    of their k-tile depth, TF32 variants with C % 32 == 0, BF16 variants with C % 64 == 0
+    and Cout % 8 == 0; never the paper family; bad ids -ENOENT."""
     from paper_2008_13145_b200 import gemm
     vid = gemm.variant_id(KernelConfig(8, 8, 8, 16, 8), "simt")
     assert lib.kp_conv3x3_supported(vid, 64, 64) == 1
@@ -204,4 +204,7 @@ def test_conv3x3_supported_query(lib):
         assert lib.kp_conv3x3_supported(tid, 48, 64) == 0  # not a whole 32-channel slab
         assert lib.kp_conv3x3_supported(tid, 64, 62) == 0
     for cfg in gemm.family_configs("bf16"):
-        assert lib.kp_conv3x3_supported(gemm.variant_id(cfg, "bf16"), 64, 64) == 0
+        bid = gemm.variant_id(cfg, "bf16")
+        assert lib.kp_conv3x3_supported(bid, 64, 64) == 1
+        assert lib.kp_conv3x3_supported(bid, 32, 64) == 0  # not a whole 64-channel slab
+        assert lib.kp_conv3x3_supported(bid, 64, 60) == 0  # weight rows not 16-byte pitched

@@ -106,3 +106,53 @@ def test_tf32_implicit_conv_equals_explicit(cuda_device, B, H, W, C, cout):
         assert torch.equal(got.view(torch.int32), ref.view(torch.int32)), (cfg.as_tuple(), gemm.k_slice_plan(vid, ProblemSize(m, k, cout, 1)))
         err = (got.double() - torch.relu(c64)).abs()
         assert bool((err <= (2 * 2.0 ** -10 + 2 * k * 2.0 ** -24) * mag + 1e-6).all()), cfg.as_tuple()
+
+
+@pytest.mark.parametrize("B,H,W,C,cout", [(2, 9, 7, 64, 64), (1, 14, 14, 64, 128), (3, 28, 28, 256, 96),
+                                         (16, 14, 14, 512, 512)])
+def test_bf16_implicit_conv_equals_explicit(cuda_device, B, H, W, C, cout):
+    """BF16 family: bf16 NHWC activations, im2col boxes of 64 channels x 128 pixels (one
+    128-byte swizzled K slab) -- bit-identical to the bf16 im2col rows of the same fp32
+    activations (kp_im2col3x3_nhwc_bf16 rounds to nearest even, as the bf16 cast) + the
+    same BF16 variant, with fused bias + ReLU."""
+    g = torch.Generator(device=cuda_device).manual_seed(B * 11 + C)
+    x = torch.randn(B, H, W, C, device=cuda_device, generator=g)
+    w = (torch.randn(9 * C, cout, device=cuda_device, generator=g) * 0.05).to(torch.bfloat16)
+    bias = torch.randn(cout, device=cuda_device, generator=g) * 0.1
+    lib = _lib.load()
+    m, k = B * H * W, 9 * C
+    cols = torch.empty(m, k, device=cuda_device, dtype=torch.bfloat16)
+    assert lib.kp_im2col3x3_nhwc_bf16(x.data_ptr(), B, H, W, C, cols.data_ptr(), k, None) == 0
+    xb = x.to(torch.bfloat16)
+    for cfg in gemm.family_configs("bf16"):
+        vid = gemm.variant_id(cfg, "bf16")
+        assert gemm.conv3x3_supported(vid, C, cout)
+        got = gemm.conv3x3(xb, w, vid, bias=bias, relu=True).reshape(-1, cout)
+        ref = torch.empty(m, cout, device=cuda_device)
+        assert lib.kp_gemm_ex(vid, m, k, cout, 1, cols.data_ptr(), k, 0, w.data_ptr(), cout, 0, ref.data_ptr(), cout, 0,
+                              bias.data_ptr(), _lib.KP_EPI_RELU, None) == 0
+        assert torch.equal(got.view(torch.int32), ref.view(torch.int32)), (cfg.as_tuple(), gemm.k_slice_plan(vid, ProblemSize(m, k, cout, 1), "bf16"))
+
+
+def test_bf16_implicit_conv_contract(cuda_device):
+    """BF16 variants need C % 64 == 0 and Cout % 8 == 0, and take bf16 operands only."""
+    vid = gemm.variant_id(gemm.family_configs("bf16")[0], "bf16")
+    assert gemm.conv3x3_supported(vid, 64, 64)
+    assert not gemm.conv3x3_supported(vid, 32, 64)
+    assert not gemm.conv3x3_supported(vid, 64, 12)
+    x = torch.zeros(1, 4, 4, 64, device=cuda_device)
+    w = torch.zeros(9 * 64, 64, device=cuda_device)
+    with pytest.raises(ValueError):
+        gemm.conv3x3(x, w, vid)  # fp32 operands on a BF16 variant
+
+
+def test_maxpool_bf16_equals_pool_then_round(cuda_device):
+    lib = _lib.load()
+    for B, H, W, C in [(2, 8, 6, 4), (3, 14, 14, 64), (1, 224, 224, 64)]:
+        x = torch.randn(B, H, W, C, device=cuda_device)
+        out = torch.empty(B, H // 2, W // 2, C, device=cuda_device, dtype=torch.bfloat16)
+        assert lib.kp_maxpool2x2_nhwc_bf16(x.data_ptr(), B, H, W, C, out.data_ptr(), None) == 0
+        want = torch.nn.functional.max_pool2d(x.permute(0, 3, 1, 2), 2).permute(0, 2, 3, 1).to(torch.bfloat16)
+        assert torch.equal(out.view(torch.int16), want.contiguous().view(torch.int16))
+    bad = torch.empty(1, 2, 2, 3, device=cuda_device)
+    assert lib.kp_maxpool2x2_nhwc_bf16(bad.data_ptr(), 1, 2, 2, 3, out.data_ptr(), None) == _lib.KP_EINVAL

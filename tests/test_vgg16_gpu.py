@@ -161,3 +161,29 @@ def test_bf16_operand_kernels(cuda_device):
     c = torch.empty(64, device=cuda_device, dtype=torch.bfloat16)
     assert lib.kp_cast_bf16(v.data_ptr(), 64, c.data_ptr(), None) == 0
     assert torch.equal(c, v.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("family,vid_col", [("bf16", 2), ("tf32", 3)])
+def test_vgg16_tensor_core_implicit_equals_explicit(cuda_device, family, vid_col):
+    """Implicit-GEMM convs on the tcgen05 families (TMA im2col boxes; BF16 reads the bf16
+    copy written by kp_cast_bf16 / kp_maxpool2x2_nhwc_bf16) give the same logits as im2col
+    + GEMM, bit for bit, eager and graph-captured, at a batch where conv rows cross images."""
+    from paper_2008_13145_b200 import gemm
+    from paper_2008_13145_b200.classify import TreeModel
+    from paper_2008_13145_b200.selection import ConfigSubset
+
+    cfgs = gemm.family_configs(family)
+    leaf = TreeModel(feature=np.array([-1]), threshold=np.array([np.nan]), left=np.array([-1]),
+                     right=np.array([-1]), leaf_class=np.array([0]))
+    disp = Dispatcher(leaf, ConfigSubset((vid_col,), "fixed", 1, 1), cfgs, family)
+    convs, fcs = vgg16.init_weights(seed=0)
+    x = torch.randn(2, 224, 224, 3, generator=torch.Generator().manual_seed(3)).to(cuda_device)
+    imp = vgg16.Vgg16(disp, 2, cuda_device, weights=(convs, fcs))
+    exp = vgg16.Vgg16(disp, 2, cuda_device, weights=(convs, fcs), implicit=False)
+    assert sum(lay[-1] for lay in imp.layers) == 12 and not any(lay[-1] for lay in exp.layers)
+    a = imp.forward(x).clone()
+    b = exp.forward(x).clone()
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+    imp.capture()
+    c = imp.forward(x).clone()
+    assert torch.equal(a.view(torch.int32), c.view(torch.int32))
