@@ -397,7 +397,7 @@ def e2e_layers(args, world, device, stream, disp, bufs, step_flops, in_dtype):
     s_handle = stream.cuda_stream
     launches = [0]
 
-    implicit = [geo[lname] is not None and not bf16 and gemm.conv3x3_supported(vid, geo[lname][1], p.n)
+    implicit = [geo[lname] is not None and gemm.conv3x3_supported(vid, geo[lname][1], p.n)
                 for (name, p, A, W, C, vid), lname in zip(bufs, names)]
 
     def lower(i, lname, p, A):
@@ -432,6 +432,10 @@ def e2e_layers(args, world, device, stream, disp, bufs, step_flops, in_dtype):
                 # implicit GEMM: the dispatched variant gathers the patches from the NHWC
                 # activation with TMA im2col copies (kp_conv3x3_nhwc_ex), no im2col pass
                 x = dev_in[i]
+                if bf16:  # BF16 family: a bf16 copy of the activation (A's rows hold m*k >= its size)
+                    _lib.check(lib.kp_cast_bf16(x.data_ptr(), x.numel(), A.data_ptr(), s_handle), "kp_cast_bf16")
+                    launches[0] += 1
+                    x = A
                 _lib.check(lib.kp_conv3x3_nhwc_ex(vid, x.data_ptr(), args.batch, g[0], g[0], g[1], W.data_ptr(), p.n,
                                                   C.data_ptr(), None, 0, s_handle), "kp_conv3x3_nhwc_ex")
             else:
@@ -465,8 +469,8 @@ def e2e_layers(args, world, device, stream, disp, bufs, step_flops, in_dtype):
             "launches_per_step": launches[0] // args.steps,
             "implicit_conv_layers": sum(implicit),
             "path": "host NHWC activations -> H2D -> conv layers: kp_conv3x3_nhwc_ex (implicit GEMM, TMA im2col) "
-                    "where the dispatched variant supports it, else kp_im2col3x3_nhwc" +
-                    (" + kp_cast_bf16" if bf16 else "") + " + Dispatcher.matmul (kp_gemm) -> D2H of every layer output"}
+                    "where the dispatched variant supports it" + (" on a kp_cast_bf16 copy" if bf16 else "") +
+                    ", else kp_im2col3x3_nhwc" + ("_bf16" if bf16 else "") + " + Dispatcher.matmul (kp_gemm) -> D2H of every layer output"}
 
 
 # ---------------------------------------------------------------------- ours --

@@ -95,8 +95,12 @@ int kp_gemm(int id, int m, int k, int n, int batch,
 /* Fused epilogue variant (VGG16 conv/fc layers):
  *   C = act(A * B + bias[col]), bias may be NULL, act = ReLU when flags & KP_EPI_RELU.
  * The bias add and ReLU follow the fp32 accumulation chain, so SIMT results stay
- * bit-exact against oracle_chain + bias -> max(0, .). */
+ * bit-exact against oracle_chain + bias -> max(0, .).
+ * KP_EPI_BF16_OUT (TF32 and BF16 variants only, else KP_EINVAL): C is bf16, the fp32
+ * epilogue result rounded to nearest even -- a BF16 layer's output written directly as
+ * the next layer's operand (equal to fp32 C followed by kp_cast_bf16). */
 #define KP_EPI_RELU 1
+#define KP_EPI_BF16_OUT 2
 int kp_gemm_ex(int id, int m, int k, int n, int batch,
                const void* A, int64_t lda, int64_t sA,
                const void* B, int64_t ldb, int64_t sB,
@@ -228,7 +232,8 @@ int kp_cast_bf16(const float* x, int64_t n, void* out, void* stream);
  * gathered straight from x by TMA im2col copies -- no im2col buffer in HBM.  Same launch
  * plan (k-slices) and accumulation order as the explicit path, so the output is
  * bit-identical.  Element types follow kp_gemm: x and w are fp32 for SIMT/TF32 variants
- * and bf16 for BF16 variants (out is fp32 for all).
+ * and bf16 for BF16 variants; out is fp32, or bf16 with flags & KP_EPI_BF16_OUT
+ * (tensor-core variants, as kp_gemm_ex).
  * kp_conv3x3_supported(id, C, Cout) returns 1 when variant id can run it (SIMT variant
  * with TMA staging, i.e. CTA tile <= 256 columns, C a multiple of its k-tile depth,
  * Cout % 4 == 0; a TF32 variant with C % 32 == 0 and Cout % 4 == 0; a BF16 variant with
@@ -236,14 +241,14 @@ int kp_cast_bf16(const float* x, int64_t n, void* out, void* stream);
  * im2col boxes into the tcgen05 ring, 1-CTA kernel), 0 when not (PAPER), < 0 for a bad
  * id.  x, w and out must be 16-byte aligned. */
 int kp_conv3x3_supported(int id, int C, int Cout);
-int kp_conv3x3_nhwc_ex(int id, const void* x, int B, int H, int W, int C, const void* w, int Cout, float* out,
+int kp_conv3x3_nhwc_ex(int id, const void* x, int B, int H, int W, int C, const void* w, int Cout, void* out,
                        const float* bias, int flags, void* stream);
 /* 2x2 / stride 2 max pooling, NHWC: (B, H, W, C) -> (B, H/2, W/2, C). */
 int kp_maxpool2x2_nhwc(const float* x, int B, int H, int W, int C, float* out, void* stream);
-/* The same pooling with a bf16 result (round to nearest even; C % 4 == 0, x 16-byte and
- * out 8-byte aligned): the BF16 family's implicit-conv operand.  Rounding is monotonic,
- * so this equals pooling in fp32 and rounding in kp_im2col3x3_nhwc_bf16. */
-int kp_maxpool2x2_nhwc_bf16(const float* x, int B, int H, int W, int C, void* out, void* stream);
+/* The same pooling of bf16 activations (the BF16 family's KP_EPI_BF16_OUT layer outputs;
+ * C % 8 == 0, x and out 16-byte aligned).  Exact: the max is one of its inputs, and
+ * rounding is monotonic, so it equals pooling in fp32 and rounding afterwards. */
+int kp_maxpool2x2_nhwc_bf16(const void* x, int B, int H, int W, int C, void* out, void* stream);
 
 #ifdef __cplusplus
 }

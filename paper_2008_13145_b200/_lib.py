@@ -23,6 +23,7 @@ KP_ENOENT = -2
 KP_EIO = -5
 KP_EINVAL = -22
 KP_EPI_RELU = 1
+KP_EPI_BF16_OUT = 2
 
 FAMILY_PAPER = 0
 FAMILY_SIMT = 1

@@ -403,6 +403,7 @@ kp::GemmArgs make_args(int m, int k, int n, int batch, const void* A, int64_t ld
   p.conv_h = p.conv_w = p.conv_c = 0;
   p.bias = nullptr;
   p.relu = 0;
+  p.c_bf16 = 0;
   return p;
 }
 
@@ -482,15 +483,28 @@ int kp_gemm(int id, int m, int k, int n, int batch, const void* A, int64_t lda, 
   return launch(id, make_args(m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC), static_cast<cudaStream_t>(stream));
 }
 
+// Epilogue flags of kp_gemm_ex / kp_conv3x3_nhwc_ex into p (id already validated).
+int apply_epilogue(int id, const float* bias, int flags, kp::GemmArgs& p) {
+  if (flags & ~(KP_EPI_RELU | KP_EPI_BF16_OUT)) return fail(KP_EINVAL, "unknown epilogue flags 0x%x", flags);
+  if (flags & KP_EPI_BF16_OUT) {
+    const int fam = registry().variants[id].family;
+    if (fam != KP_FAMILY_TF32 && fam != KP_FAMILY_BF16)
+      return fail(KP_EINVAL, "KP_EPI_BF16_OUT needs a tensor-core variant (TF32 or BF16), variant %d is not", id);
+    p.c_bf16 = 1;
+  }
+  p.bias = bias;
+  p.relu = (flags & KP_EPI_RELU) != 0;
+  return KP_OK;
+}
+
 int kp_gemm_ex(int id, int m, int k, int n, int batch, const void* A, int64_t lda, int64_t sA, const void* B,
                int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, const float* bias, int flags,
                void* stream) {
   int rc = check_problem(id, m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC);
   if (rc != KP_OK) return rc;
-  if (flags & ~KP_EPI_RELU) return fail(KP_EINVAL, "unknown epilogue flags 0x%x", flags);
   kp::GemmArgs p = make_args(m, k, n, batch, A, lda, sA, B, ldb, sB, C, ldc, sC);
-  p.bias = bias;
-  p.relu = (flags & KP_EPI_RELU) != 0;
+  rc = apply_epilogue(id, bias, flags, p);
+  if (rc != KP_OK) return rc;
   return launch(id, p, static_cast<cudaStream_t>(stream));
 }
 
@@ -509,7 +523,7 @@ int kp_conv3x3_supported(int id, int C, int Cout) {
   return (e.tma_ok && C % e.bk == 0 && Cout % 4 == 0) ? 1 : 0;
 }
 
-int kp_conv3x3_nhwc_ex(int id, const void* x, int B, int H, int W, int C, const void* w, int Cout, float* out,
+int kp_conv3x3_nhwc_ex(int id, const void* x, int B, int H, int W, int C, const void* w, int Cout, void* out,
                        const float* bias, int flags, void* stream) {
   if (B < 1 || H < 1 || W < 1 || C < 1 || Cout < 1) return fail(KP_EINVAL, "conv dims must be >= 1");
   if (static_cast<int64_t>(B) * H * W > 0x7fffffffLL || 9LL * C > 0x7fffffffLL)
@@ -520,14 +534,13 @@ int kp_conv3x3_nhwc_ex(int id, const void* x, int B, int H, int W, int C, const 
   if (!x || !w || !out) return fail(KP_EINVAL, "null operand pointer");
   auto aligned = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) % 16) == 0; };
   if (!aligned(x) || !aligned(w) || !aligned(out)) return fail(KP_EINVAL, "x, w and out must be 16-byte aligned");
-  if (flags & ~KP_EPI_RELU) return fail(KP_EINVAL, "unknown epilogue flags 0x%x", flags);
   const int m = B * H * W, k = 9 * C;
   kp::GemmArgs p = make_args(m, k, Cout, 1, x, k, 0, w, Cout, 0, out, Cout, 0);
+  const int erc = apply_epilogue(id, bias, flags, p);
+  if (erc != KP_OK) return erc;
   p.conv_h = H;
   p.conv_w = W;
   p.conv_c = C;
-  p.bias = bias;
-  p.relu = (flags & KP_EPI_RELU) != 0;
   return launch(id, p, static_cast<cudaStream_t>(stream));
 }
 
@@ -714,11 +727,11 @@ int kp_maxpool2x2_nhwc(const float* x, int B, int H, int W, int C, float* out, v
   return e == cudaSuccess ? KP_OK : cuda_fail(e, "maxpool launch");
 }
 
-int kp_maxpool2x2_nhwc_bf16(const float* x, int B, int H, int W, int C, void* out, void* stream) {
+int kp_maxpool2x2_nhwc_bf16(const void* x, int B, int H, int W, int C, void* out, void* stream) {
   if (!x || !out) return fail(KP_EINVAL, "null pointer");
-  if (B < 1 || H < 2 || W < 2 || C < 1 || C % 4 != 0) return fail(KP_EINVAL, "bad activation shape (C % 4 == 0)");
+  if (B < 1 || H < 2 || W < 2 || C < 1 || C % 8 != 0) return fail(KP_EINVAL, "bad activation shape (C % 8 == 0)");
   cudaError_t e = kp::maxpool2_nhwc_bf16_launch(x, B, H, W, C, out, static_cast<cudaStream_t>(stream));
-  return e == cudaSuccess ? KP_OK : cuda_fail(e, "maxpool (bf16 out) launch (x 16-byte, out 8-byte aligned)");
+  return e == cudaSuccess ? KP_OK : cuda_fail(e, "maxpool (bf16) launch (x and out 16-byte aligned)");
 }
 
 int kp_dispatch_load(int n_nodes, const int32_t* feature, const double* threshold, const int32_t* left,

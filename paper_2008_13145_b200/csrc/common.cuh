@@ -1,6 +1,7 @@
 // Shared device helpers and launch-parameter structs for the kpgemm families.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -26,6 +27,9 @@ struct GemmArgs {
   // Fused epilogue (kp_gemm_ex): C = act(A*B + bias[col]); bias may be null.
   const float* bias;
   int relu;
+  // Tensor-core families only (KP_EPI_BF16_OUT): C is bf16, the epilogue result rounded
+  // to nearest even -- the operand the next BF16 layer reads, no separate cast pass.
+  int c_bf16;
   // k-slicing (SIMT family, planned by capi.cu): the k-tiles are cut into kslices
   // consecutive ranges of kt_per_slice tiles; slice z is computed by the CTA at
   // blockIdx.z of a (1, 1, kslices) thread-block cluster and the partial tiles are
@@ -50,6 +54,12 @@ __device__ __forceinline__ float epilogue(const GemmArgs& p, float v, int64_t co
   if (p.bias) v = v + __ldg(p.bias + col);
   if (p.relu) v = fmaxf(v, 0.0f);
   return v;
+}
+
+// Two fp32 values rounded to nearest even and packed as bf16 (lo in the low half).
+__device__ __forceinline__ unsigned pack_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const unsigned*>(&v);
 }
 
 // ---- vector load / store of N consecutive floats (N in {1,2,4,8}) ---------

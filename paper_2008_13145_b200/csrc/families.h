@@ -60,7 +60,7 @@ cudaError_t im2col3x3_nhwc_pad_launch(const float* x, int B, int H, int W, int C
                                       cudaStream_t s);
 cudaError_t im2col3x3_nhwc_bf16_launch(const float* x, int B, int H, int W, int C, void* out, int kpad,
                                        cudaStream_t s);
-cudaError_t maxpool2_nhwc_bf16_launch(const float* x, int B, int H, int W, int C, void* out, cudaStream_t s);
+cudaError_t maxpool2_nhwc_bf16_launch(const void* x, int B, int H, int W, int C, void* out, cudaStream_t s);
 cudaError_t cast_bf16_launch(const float* x, int64_t n, void* out, cudaStream_t s);
 // Copy batch x rows x cols elements (es bytes each; source pitch ld, batch stride sbatch)
 // into rows pitched to ldd (a multiple of 16 bytes), batch stride rows * ldd.

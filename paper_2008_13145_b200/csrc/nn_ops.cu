@@ -12,11 +12,6 @@
 namespace kp {
 namespace {
 
-__device__ __forceinline__ unsigned pack_bf16x2(float lo, float hi) {
-  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo (low half), .y = hi
-  return *reinterpret_cast<const unsigned*>(&v);
-}
-
 // One thread per output element; consecutive threads walk k = (dy*3 + dx)*C + c, so
 // both the gather (contiguous channels of one tap) and the store are coalesced.
 __global__ void im2col3x3_nhwc_kernel(const float* __restrict__ x, int B, int H, int W, int C,
@@ -166,24 +161,32 @@ __global__ void maxpool2_nhwc_vec4_kernel(const float4* __restrict__ x, int B, i
   }
 }
 
-// 2x2 / stride 2 max pool of fp32 NHWC activations written as bf16 (round to nearest even):
-// the BF16 family's implicit-conv operand.  rn() is monotonic, so rn(max) == max(rn) and
-// this equals pooling first and rounding in the next layer's bf16 im2col (C % 4 == 0).
-__global__ void maxpool2_nhwc_bf16_kernel(const float4* __restrict__ x, int B, int H, int W, int C4,
-                                          uint2* __restrict__ out, unsigned total) {
+// 2x2 / stride 2 max pool of bf16 NHWC activations (BF16 family, written by the GEMM
+// epilogue with KP_EPI_BF16_OUT), 8 channels per thread (C % 8 == 0).  The max of four
+// bf16 values is one of them, so the result is exact.
+__device__ __forceinline__ unsigned max_bf16x2(unsigned a, unsigned b) {
+  __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&a), y = *reinterpret_cast<const __nv_bfloat162*>(&b);
+  const __nv_bfloat162 r = __hmax2(x, y);
+  return *reinterpret_cast<const unsigned*>(&r);
+}
+
+__global__ void maxpool2_nhwc_bf16_kernel(const uint4* __restrict__ x, int B, int H, int W, int C8,
+                                          uint4* __restrict__ out, unsigned total) {
   const unsigned Ho = H / 2, Wo = W / 2;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const unsigned c4 = i % C4;
-    unsigned r = i / C4;
+    const unsigned c8 = i % C8;
+    unsigned r = i / C8;
     const unsigned wo = r % Wo;
     r /= Wo;
     const unsigned ho = r % Ho;
     const unsigned b = r / Ho;
-    const float4* base = x + ((static_cast<int64_t>(b) * H + 2 * ho) * W + 2 * wo) * C4 + c4;
-    const float4 a0 = __ldg(base), a1 = __ldg(base + C4);
-    const float4 a2 = __ldg(base + static_cast<int64_t>(W) * C4), a3 = __ldg(base + static_cast<int64_t>(W) * C4 + C4);
-    out[i] = make_uint2(pack_bf16x2(fmaxf(fmaxf(a0.x, a1.x), fmaxf(a2.x, a3.x)), fmaxf(fmaxf(a0.y, a1.y), fmaxf(a2.y, a3.y))),
-                        pack_bf16x2(fmaxf(fmaxf(a0.z, a1.z), fmaxf(a2.z, a3.z)), fmaxf(fmaxf(a0.w, a1.w), fmaxf(a2.w, a3.w))));
+    const uint4* base = x + ((static_cast<int64_t>(b) * H + 2 * ho) * W + 2 * wo) * C8 + c8;
+    const uint4 a0 = __ldg(base), a1 = __ldg(base + C8);
+    const uint4 a2 = __ldg(base + static_cast<int64_t>(W) * C8), a3 = __ldg(base + static_cast<int64_t>(W) * C8 + C8);
+    out[i] = make_uint4(max_bf16x2(max_bf16x2(a0.x, a1.x), max_bf16x2(a2.x, a3.x)),
+                        max_bf16x2(max_bf16x2(a0.y, a1.y), max_bf16x2(a2.y, a3.y)),
+                        max_bf16x2(max_bf16x2(a0.z, a1.z), max_bf16x2(a2.z, a3.z)),
+                        max_bf16x2(max_bf16x2(a0.w, a1.w), max_bf16x2(a2.w, a3.w)));
   }
 }
 
@@ -297,17 +300,15 @@ cudaError_t maxpool2_nhwc_launch(const float* x, int B, int H, int W, int C, flo
   return cudaGetLastError();
 }
 
-cudaError_t maxpool2_nhwc_bf16_launch(const float* x, int B, int H, int W, int C, void* out, cudaStream_t s) {
+cudaError_t maxpool2_nhwc_bf16_launch(const void* x, int B, int H, int W, int C, void* out, cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(B) * (H / 2) * (W / 2) * C;
-  if (C % 4 != 0 || !aligned16(x) || (reinterpret_cast<uintptr_t>(out) % 8) != 0 || total / 4 >= 0x7fffffffLL)
-    return cudaErrorInvalidValue;
-  const unsigned t4 = static_cast<unsigned>(total / 4);
-  if (t4 == 0) return cudaSuccess;
-  maxpool2_nhwc_bf16_kernel<<<grid_for(t4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(x), B, H, W, C / 4,
-                                                                reinterpret_cast<uint2*>(out), t4);
+  if (C % 8 != 0 || !aligned16(x) || !aligned16(out) || total / 8 >= 0x7fffffffLL) return cudaErrorInvalidValue;
+  const unsigned t8 = static_cast<unsigned>(total / 8);
+  if (t8 == 0) return cudaSuccess;
+  maxpool2_nhwc_bf16_kernel<<<grid_for(t8, 256), 256, 0, s>>>(static_cast<const uint4*>(x), B, H, W, C / 8,
+                                                                static_cast<uint4*>(out), t8);
   return cudaGetLastError();
 }
-
 
 cudaError_t repack_rows_launch(const void* src, int64_t ld, int64_t sbatch, int rows, int cols, int batch, int es,
                                void* dst, int64_t ldd, cudaStream_t s) {

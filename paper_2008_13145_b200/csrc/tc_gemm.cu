@@ -288,6 +288,18 @@ __device__ __forceinline__ void tc_slice_reduce(const GemmArgs& p, float* part, 
       for (int e = 0; e < 4; ++e)
         if (col + e < p.n) o[e] = epilogue(p, o[e], col + e);
     }
+    if (p.c_bf16) {
+      __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(p.C) + static_cast<int64_t>(b) * p.sC +
+                          static_cast<int64_t>(row) * p.ldc + col;
+      if (p.c_vec && col + 4 <= p.n) {
+        *reinterpret_cast<uint2*>(ob) = make_uint2(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (col + e < p.n) ob[e] = __float2bfloat16_rn(o[e]);
+      }
+      continue;
+    }
     float* out = Cb + static_cast<int64_t>(row) * p.ldc + col;
     if (p.c_vec && col + 4 <= p.n) {
       *reinterpret_cast<float4*>(out) = make_float4(o[0], o[1], o[2], o[3]);
@@ -478,7 +490,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int e = 0; e < 16; ++e)
               if (col + e < p.n) v[e] = epilogue(p, v[e], col + e);
           }
-          if (p.c_vec && col + 16 <= p.n) {
+          if (p.c_bf16) {
+            __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(p.C) + static_cast<int64_t>(b) * p.sC +
+                                static_cast<int64_t>(row) * p.ldc + col;
+            if (p.c_vec && col + 16 <= p.n) {
+              uint32_t w[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) w[q] = pack_bf16x2(v[2 * q], v[2 * q + 1]);
+              reinterpret_cast<uint4*>(ob)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+              reinterpret_cast<uint4*>(ob)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (col + e < p.n) ob[e] = __float2bfloat16_rn(v[e]);
+            }
+          } else if (p.c_vec && col + 16 <= p.n) {
 #pragma unroll
             for (int q = 0; q < 4; ++q)
               *reinterpret_cast<float4*>(out + col + 4 * q) =
@@ -916,7 +942,8 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   }
   GemmArgs p = p0;
   auto aligned = [](const void* ptr, int bytes) { return (reinterpret_cast<uintptr_t>(ptr) % bytes) == 0; };
-  p.c_vec = (p.ldc % 4 == 0) && (p.sC % 4 == 0) && aligned(p.C, 16);
+  p.c_vec = p.c_bf16 ? (p.ldc % 8 == 0) && (p.sC % 8 == 0) && aligned(p.C, 16)
+                     : (p.ldc % 4 == 0) && (p.sC % 4 == 0) && aligned(p.C, 16);
   const int tiles_m = (p.m + BM - 1) / BM, tiles_n = (p.n + BN - 1) / BN;
   const int64_t n_tiles = static_cast<int64_t>(tiles_m) * tiles_n * p.batch;
   if (n_tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
@@ -943,7 +970,7 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   CUtensorMap mc;
   std::memset(&mc, 0, sizeof(mc));
   int tma_store = 0;
-  if (p.kslices <= 1 && p.c_vec && p.k <= kTmaStoreMaxK) {
+  if (p.kslices <= 1 && p.c_vec && !p.c_bf16 && p.k <= kTmaStoreMaxK) {
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.n), static_cast<cuuint64_t>(p.m),
                           static_cast<cuuint64_t>(p.batch)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.ldc) * 4,
@@ -1009,7 +1036,7 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   }
   if constexpr (PAIR_STAGES > 0) {
     // CTA pairs for persistent TMA launches (no tail split: the pair kernel runs every tile)
-    if (!lsu && p.kslices <= 1 && p.conv_c == 0)
+    if (!lsu && p.kslices <= 1 && p.conv_c == 0 && !p.c_bf16)
       return launch_pair<kTF32, BN, PAIR_STAGES>(p, ma, mb, mc, a_batched, b_batched, tma_store, s);
     tail = 0;
   }

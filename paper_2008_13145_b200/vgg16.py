@@ -10,10 +10,11 @@ random (no network access for trained weights), seeded, identical on every rank.
 
 Convolutions whose dispatched variant supports it run as implicit GEMMs instead
 (``kp_conv3x3_nhwc_ex``: TMA im2col copies gather the patches from the activation, no
-im2col buffer).  The BF16 family keeps fp32 activations between layers (the GEMM epilogue
-writes fp32); its implicit convs read a bf16 copy made by ``kp_cast_bf16`` or, after a
-pool, by ``kp_maxpool2x2_nhwc_bf16`` -- the same round-to-nearest of the same fp32 values
-the explicit path's bf16 im2col applies, so both paths give identical logits.
+im2col buffer).  On the BF16 family, when every conv after conv1_1 is implicit, the
+activations are bf16 end to end: each GEMM epilogue rounds its output to bf16
+(``KP_EPI_BF16_OUT``) and pooling runs on bf16 (``kp_maxpool2x2_nhwc_bf16``).  Otherwise
+activations are fp32 and a BF16 layer rounds its input in the bf16 im2col / cast.  Both
+are the same round-to-nearest of the same fp32 values, so the logits are identical.
 
 Data parallelism (configs[2] at 1/2/4/8 GPUs): each rank runs its own images with
 replicated weights; there is no collective on the data path.  The whole forward for a
@@ -94,17 +95,23 @@ class Vgg16:
             vid = self.disp.variant(ProblemSize(m, k, cout, 1))
             implicit = self.implicit and gemm.conv3x3_supported(vid, cin, cout)
             self.layers.append((B, H, cin, cout, m, k_launch, vid, implicit))
+        # BF16 family with every conv after conv1_1 implicit: activations stay bf16 end to end
+        # -- each GEMM epilogue rounds its output (KP_EPI_BF16_OUT), pools run on bf16 -- the
+        # same roundings of the same fp32 values as the fp32-activation path below
+        self.bf16_acts = self.bf16 and all(lay[-1] for lay in self.layers[1:])
         # ping-pong activation buffers sized for the largest layer output (B*224*224*64)
         act = B * 224 * 224 * 64
-        self.act = [torch.empty(act, device=self.device) for _ in range(2)]
+        self.act = [torch.empty(8 if self.bf16_acts else act, device=self.device) for _ in range(2)]
         # im2col rows for the explicit layers only (conv1_1 alone when the rest are implicit)
         cols = max([m * k for (_, _, _, _, m, k, _, imp) in self.layers if not imp], default=8)
         self.cols = torch.empty(cols, device=self.device, dtype=wdt)
-        # bf16 copy of an implicit conv's input (BF16 family)
-        self.act16 = (torch.empty(act, device=self.device, dtype=torch.bfloat16)
-                      if self.bf16 and any(lay[-1] for lay in self.layers) else None)
+        # bf16 activations: the ping-pong pair (bf16_acts), else one bf16 copy of an
+        # implicit conv's fp32 input (kp_cast_bf16 / a bf16 pool)
+        n16 = 2 if self.bf16_acts else 1 if self.bf16 and any(lay[-1] for lay in self.layers) else 0
+        self.act16 = [torch.empty(act, device=self.device, dtype=torch.bfloat16) for _ in range(n16)]
         self.fc_in = torch.empty(B, 7 * 7 * 512, device=self.device, dtype=wdt)  # bf16 fc operands
         self.fc_in2 = torch.empty(B, 4096, device=self.device, dtype=wdt)
+        self.fc16 = [torch.empty(B, 4096, device=self.device, dtype=wdt) for _ in range(2 if self.bf16_acts else 0)]
         self.input = torch.empty(B, 224, 224, 3, device=self.device)
         self.logits = torch.empty(B, 1000, device=self.device)
         self.fc_buf = [torch.empty(B, 4096, device=self.device) for _ in range(2)]
@@ -123,32 +130,65 @@ class Vgg16:
         out += [ProblemSize(B, fin, fout, 1) for fin, fout, _ in VGG16_FC]
         return out
 
-    def _gemm(self, A, W, bias, C, m, k, n, relu, stream):
+    def _gemm(self, A, W, bias, C, m, k, n, relu, stream, flags=0):
         lib = _lib.load()
         vid = self.disp.variant(ProblemSize(m, k, n, 1))
         _lib.check(lib.kp_gemm_ex(vid, m, k, n, 1, A.data_ptr(), k, 0, W.data_ptr(), n, 0, C.data_ptr(), n, 0,
-                                  bias.data_ptr(), _lib.KP_EPI_RELU if relu else 0, stream),
+                                  bias.data_ptr(), flags | (_lib.KP_EPI_RELU if relu else 0), stream),
                    f"kp_gemm_ex({m},{k},{n})")
         return vid
 
+    def _forward_bf16(self, stream_handle):
+        """BF16 activations end to end: conv1_1 by bf16 im2col + GEMM, every other conv an
+        implicit GEMM, each writing bf16 (KP_EPI_BF16_OUT); bf16 pools; fc6/fc7 bf16 out,
+        fc8 fp32 logits."""
+        lib = _lib.load()
+        B, H, C = self.batch, 224, 3
+        src = self.input  # fp32: only conv1_1's im2col reads it
+        di = 0
+        ci = 0
+        out16 = _lib.KP_EPI_RELU | _lib.KP_EPI_BF16_OUT
+        for pi, item in enumerate(VGG16_PLAN):
+            if item == "M":
+                dst = self.fc_in if pi == len(VGG16_PLAN) - 1 else self.act16[di]
+                _lib.check(lib.kp_maxpool2x2_nhwc_bf16(src.data_ptr(), B, H, H, C, dst.data_ptr(), stream_handle),
+                           "kp_maxpool2x2_nhwc_bf16")
+                H //= 2
+            else:
+                _, _, cin, cout, m, k, vid, implicit = self.layers[ci]
+                w, b = self.convs[ci]
+                ci += 1
+                dst = self.act16[di]
+                if implicit:
+                    _lib.check(lib.kp_conv3x3_nhwc_ex(vid, src.data_ptr(), B, H, H, cin, w.data_ptr(), cout,
+                                                      dst.data_ptr(), b.data_ptr(), out16, stream_handle),
+                               f"kp_conv3x3_nhwc_ex({B}x{H}x{H}x{cin} -> {cout}, bf16 out)")
+                else:  # conv1_1 (C = 3): bf16 im2col rows of the fp32 input
+                    _lib.check(lib.kp_im2col3x3_nhwc_bf16(src.data_ptr(), B, H, H, cin, self.cols.data_ptr(), k,
+                                                          stream_handle), "kp_im2col3x3_nhwc_bf16")
+                    self._gemm(self.cols, w, b, dst, m, k, cout, True, stream_handle, _lib.KP_EPI_BF16_OUT)
+                C = cout
+            src = dst
+            di ^= 1
+        x = self.fc_in
+        for j, ((fin, fout, relu), (w, b)) in enumerate(zip(VGG16_FC, self.fcs)):
+            last = j == len(self.fcs) - 1
+            out = self.logits if last else self.fc16[j % 2]
+            self._gemm(x, w, b, out, B, fin, fout, relu, stream_handle, 0 if last else _lib.KP_EPI_BF16_OUT)
+            x = out
+        return self.logits
+
     def _forward(self, stream_handle):
+        if self.bf16_acts:
+            return self._forward_bf16(stream_handle)
         lib = _lib.load()
         B, H, C = self.batch, 224, 3
         src = self.input
-        src16 = False  # act16 already holds src rounded to bf16 (a bf16 pool wrote it)
         dst_i = 0
         ci = 0
-        for pi, item in enumerate(VGG16_PLAN):
+        for item in VGG16_PLAN:
             dst = self.act[dst_i]
             if item == "M":
-                nxt = ci if pi + 1 < len(VGG16_PLAN) and VGG16_PLAN[pi + 1] != "M" else None
-                if self.act16 is not None and nxt is not None and nxt < len(self.layers) and self.layers[nxt][-1]:
-                    # the next conv is an implicit BF16 GEMM: pool straight into its bf16 operand
-                    _lib.check(lib.kp_maxpool2x2_nhwc_bf16(src.data_ptr(), B, H, H, C, self.act16.data_ptr(),
-                                                           stream_handle), "kp_maxpool2x2_nhwc_bf16")
-                    src16 = True
-                    H //= 2
-                    continue
                 _lib.check(lib.kp_maxpool2x2_nhwc(src.data_ptr(), B, H, H, C, dst.data_ptr(), stream_handle),
                            "kp_maxpool2x2_nhwc")
                 H //= 2
@@ -159,11 +199,10 @@ class Vgg16:
                 if implicit:
                     # implicit GEMM: TMA im2col copies gather the patches from the activation
                     x = src
-                    if self.bf16:
-                        if not src16:
-                            _lib.check(lib.kp_cast_bf16(src.data_ptr(), B * H * H * cin, self.act16.data_ptr(),
-                                                        stream_handle), "kp_cast_bf16")
-                        x = self.act16
+                    if self.bf16:  # a bf16 copy of the fp32 activation
+                        _lib.check(lib.kp_cast_bf16(src.data_ptr(), B * H * H * cin, self.act16[0].data_ptr(),
+                                                    stream_handle), "kp_cast_bf16")
+                        x = self.act16[0]
                     _lib.check(lib.kp_conv3x3_nhwc_ex(vid, x.data_ptr(), B, H, H, cin, w.data_ptr(), cout,
                                                       dst.data_ptr(), b.data_ptr(), _lib.KP_EPI_RELU, stream_handle),
                                f"kp_conv3x3_nhwc_ex({B}x{H}x{H}x{cin} -> {cout})")
@@ -180,7 +219,6 @@ class Vgg16:
                                                      stream_handle), "kp_im2col3x3_nhwc")
                     self._gemm(self.cols, w, b, dst, m, k, cout, True, stream_handle)
                 C = cout
-                src16 = False
             src = dst
             dst_i ^= 1
         x = src  # (B, 7, 7, 512) NHWC flattened per image = fc6 input rows

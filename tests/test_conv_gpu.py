@@ -147,12 +147,53 @@ def test_bf16_implicit_conv_contract(cuda_device):
 
 
 def test_maxpool_bf16_equals_pool_then_round(cuda_device):
+    """bf16 pooling is exact: pooling the rounded activations equals rounding the fp32 pool."""
     lib = _lib.load()
-    for B, H, W, C in [(2, 8, 6, 4), (3, 14, 14, 64), (1, 224, 224, 64)]:
+    for B, H, W, C in [(2, 8, 6, 8), (3, 14, 14, 64), (1, 224, 224, 64)]:
         x = torch.randn(B, H, W, C, device=cuda_device)
+        xb = x.to(torch.bfloat16)
         out = torch.empty(B, H // 2, W // 2, C, device=cuda_device, dtype=torch.bfloat16)
-        assert lib.kp_maxpool2x2_nhwc_bf16(x.data_ptr(), B, H, W, C, out.data_ptr(), None) == 0
+        assert lib.kp_maxpool2x2_nhwc_bf16(xb.data_ptr(), B, H, W, C, out.data_ptr(), None) == 0
         want = torch.nn.functional.max_pool2d(x.permute(0, 3, 1, 2), 2).permute(0, 2, 3, 1).to(torch.bfloat16)
         assert torch.equal(out.view(torch.int16), want.contiguous().view(torch.int16))
-    bad = torch.empty(1, 2, 2, 3, device=cuda_device)
-    assert lib.kp_maxpool2x2_nhwc_bf16(bad.data_ptr(), 1, 2, 2, 3, out.data_ptr(), None) == _lib.KP_EINVAL
+    bad = torch.empty(1, 2, 2, 4, device=cuda_device, dtype=torch.bfloat16)
+    assert lib.kp_maxpool2x2_nhwc_bf16(bad.data_ptr(), 1, 2, 2, 4, out.data_ptr(), None) == _lib.KP_EINVAL
+
+
+@pytest.mark.parametrize("family", ["bf16", "tf32"])
+def test_bf16_out_epilogue_equals_cast(cuda_device, family):
+    """KP_EPI_BF16_OUT writes the fp32 epilogue result rounded to bf16 (nearest even) --
+    equal to the fp32 output of the same variant cast afterwards -- on the persistent path
+    (direct stores, TMA stores disabled), k-sliced launches (DSMEM reduction stores), the
+    tail split, ragged n, and the implicit conv; SIMT variants reject the flag."""
+    lib = _lib.load()
+    dt = gemm.input_dtype(family)
+    g = torch.Generator(device=cuda_device).manual_seed(5)
+    shapes = [(1000, 512, 256), (16, 4096, 1000), (64, 25088, 512), (3000, 96, 72)]
+    for ci, cfg in enumerate(gemm.family_configs(family)):
+        vid = gemm.variant_id(cfg, family)
+        for (m, k, n) in shapes[ci % 2::2] if ci > 1 else shapes:
+            A = torch.randn(m, k, device=cuda_device, generator=g).to(dt)
+            B = (torch.randn(k, n, device=cuda_device, generator=g) * 0.05).to(dt)
+            bias = torch.randn(n, device=cuda_device, generator=g)
+            ref = torch.empty(m, n, device=cuda_device)
+            out = torch.empty(m, n, device=cuda_device, dtype=torch.bfloat16)
+            assert lib.kp_gemm_ex(vid, m, k, n, 1, A.data_ptr(), k, 0, B.data_ptr(), n, 0, ref.data_ptr(), n, 0,
+                                  bias.data_ptr(), _lib.KP_EPI_RELU, None) == 0
+            assert lib.kp_gemm_ex(vid, m, k, n, 1, A.data_ptr(), k, 0, B.data_ptr(), n, 0, out.data_ptr(), n, 0,
+                                  bias.data_ptr(), _lib.KP_EPI_RELU | _lib.KP_EPI_BF16_OUT, None) == 0
+            assert torch.equal(out.view(torch.int16), ref.to(torch.bfloat16).view(torch.int16)), (cfg.as_tuple(), m, k, n)
+    vid = gemm.variant_id(gemm.family_configs(family)[0], family)
+    x = torch.randn(2, 14, 14, 64, device=cuda_device, generator=g).to(dt)
+    w = (torch.randn(9 * 64, 128, device=cuda_device, generator=g) * 0.05).to(dt)
+    ref = torch.empty(2, 14, 14, 128, device=cuda_device)
+    out = torch.empty(2, 14, 14, 128, device=cuda_device, dtype=torch.bfloat16)
+    assert lib.kp_conv3x3_nhwc_ex(vid, x.data_ptr(), 2, 14, 14, 64, w.data_ptr(), 128, ref.data_ptr(), None,
+                                  _lib.KP_EPI_RELU, None) == 0
+    assert lib.kp_conv3x3_nhwc_ex(vid, x.data_ptr(), 2, 14, 14, 64, w.data_ptr(), 128, out.data_ptr(), None,
+                                  _lib.KP_EPI_RELU | _lib.KP_EPI_BF16_OUT, None) == 0
+    assert torch.equal(out.view(torch.int16), ref.to(torch.bfloat16).view(torch.int16))
+    sid = gemm.variant_id(KernelConfig(8, 8, 8, 16, 8), "simt")
+    A = torch.zeros(8, 8, device=cuda_device)
+    assert lib.kp_gemm_ex(sid, 8, 8, 8, 1, A.data_ptr(), 8, 0, A.data_ptr(), 8, 0, A.data_ptr(), 8, 0, None,
+                          _lib.KP_EPI_BF16_OUT, None) == _lib.KP_EINVAL

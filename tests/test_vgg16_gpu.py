@@ -165,9 +165,10 @@ def test_bf16_operand_kernels(cuda_device):
 
 @pytest.mark.parametrize("family,vid_col", [("bf16", 2), ("tf32", 3)])
 def test_vgg16_tensor_core_implicit_equals_explicit(cuda_device, family, vid_col):
-    """Implicit-GEMM convs on the tcgen05 families (TMA im2col boxes; BF16 reads the bf16
-    copy written by kp_cast_bf16 / kp_maxpool2x2_nhwc_bf16) give the same logits as im2col
-    + GEMM, bit for bit, eager and graph-captured, at a batch where conv rows cross images."""
+    """Implicit-GEMM convs on the tcgen05 families (TMA im2col boxes; BF16 with bf16
+    activations end to end: KP_EPI_BF16_OUT epilogues and bf16 pools) give the same logits
+    as fp32 activations + im2col + GEMM, bit for bit, eager and graph-captured, at a batch
+    where conv rows cross images."""
     from paper_2008_13145_b200 import gemm
     from paper_2008_13145_b200.classify import TreeModel
     from paper_2008_13145_b200.selection import ConfigSubset
@@ -181,6 +182,7 @@ def test_vgg16_tensor_core_implicit_equals_explicit(cuda_device, family, vid_col
     imp = vgg16.Vgg16(disp, 2, cuda_device, weights=(convs, fcs))
     exp = vgg16.Vgg16(disp, 2, cuda_device, weights=(convs, fcs), implicit=False)
     assert sum(lay[-1] for lay in imp.layers) == 12 and not any(lay[-1] for lay in exp.layers)
+    assert imp.bf16_acts == (family == "bf16") and not exp.bf16_acts  # BF16: bf16 activations end to end
     a = imp.forward(x).clone()
     b = exp.forward(x).clone()
     assert torch.equal(a.view(torch.int32), b.view(torch.int32))
