@@ -203,10 +203,7 @@ __device__ __forceinline__ void f1_slice_reduce(const GemmArgs& p, float* smem, 
       }
       float o[4] = {v.x, v.y, v.z, v.w};
       float* out = Cb + row * p.ldc + col;
-      if (p.bias || p.relu) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) o[e] = (col + e < n) ? epilogue(p, o[e], col + e) : o[e];
-      }
+      if (p.bias || p.relu) epilogue_run<4>(p, o, col);
       if (p.c_vec4 && col + 4 <= n) {
         stg_vec<4>(out, o);
       } else {
@@ -482,6 +479,15 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
     return;
   }
 
+  // the thread's C bias values, fetched once up front (independent loads) instead of one
+  // dependent load per output element; epilogue() order: + bias, then ReLU
+  float bcol[C];
+#pragma unroll
+  for (int cv = 0; cv < C / VC; ++cv) {
+    const int64_t col = n0 + tcol(cv);
+#pragma unroll
+    for (int e = 0; e < VC; ++e) bcol[cv * VC + e] = (p.bias && col + e < n) ? __ldg(p.bias + col + e) : 0.0f;
+  }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t row = m0 + trow(r);
@@ -495,7 +501,8 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
       for (int e = 0; e < VC; ++e) {
         const float2 pr = acc[r][(cv * VC + e) / 2];
         v[e] = ((cv * VC + e) & 1) ? pr.y : pr.x;
-        if (p.bias || p.relu) v[e] = (col + e < n) ? epilogue(p, v[e], col + e) : v[e];
+        if (p.bias) v[e] = v[e] + bcol[cv * VC + e];
+        if (p.relu) v[e] = fmaxf(v[e], 0.0f);
       }
       if (p.c_vec && col + VC <= n) {
         stg_vec<VC>(out + col, v);

@@ -283,11 +283,7 @@ __device__ __forceinline__ void tc_slice_reduce(const GemmArgs& p, float* part, 
       v.x = v.x + w.x; v.y = v.y + w.y; v.z = v.z + w.z; v.w = v.w + w.w;
     }
     float o[4] = {v.x, v.y, v.z, v.w};
-    if (p.bias || p.relu) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (col + e < p.n) o[e] = epilogue(p, o[e], col + e);
-    }
+    if (p.bias || p.relu) epilogue_run<4>(p, o, col);
     if (p.c_bf16) {
       __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(p.C) + static_cast<int64_t>(b) * p.sC +
                           static_cast<int64_t>(row) * p.ldc + col;
@@ -451,11 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float v[32];
           tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * BN + c, v);
           tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * BN + c + 16, v + 16);
-          if (p.bias || p.relu) {
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (n0 + c + e < p.n) v[e] = epilogue(p, v[e], n0 + c + e);
-          }
+          if (p.bias || p.relu) epilogue_run<32>(p, v, n0 + c);
           uint8_t* box = stage + (epi_box & 1) * (32 * 32 * 4);
           if (lane == 0) bulk_wait_read<1>();  // the store that last used this box has read it
           __syncwarp();
@@ -485,11 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             *reinterpret_cast<float4*>(part + c + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         } else if (row < p.m) {
           const int col = n0 + c;
-          if (p.bias || p.relu) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e)
-              if (col + e < p.n) v[e] = epilogue(p, v[e], col + e);
-          }
+          if (p.bias || p.relu) epilogue_run<16>(p, v, col);
           if (p.c_bf16) {
             __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(p.C) + static_cast<int64_t>(b) * p.sC +
                                 static_cast<int64_t>(row) * p.ldc + col;
@@ -748,11 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float v[32];
           tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * BN + c, v);
           tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * BN + c + 16, v + 16);
-          if (p.bias || p.relu) {
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (n0 + c + e < p.n) v[e] = epilogue(p, v[e], n0 + c + e);
-          }
+          if (p.bias || p.relu) epilogue_run<32>(p, v, n0 + c);
           uint8_t* box = stage + (epi_box & 1) * (32 * 32 * 4);
           if (lane == 0) bulk_wait_read<1>();
           __syncwarp();
@@ -774,11 +758,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * BN + c, v);
           if (row < p.m) {
             const int col = n0 + c;
-            if (p.bias || p.relu) {
-#pragma unroll
-              for (int e = 0; e < 16; ++e)
-                if (col + e < p.n) v[e] = epilogue(p, v[e], col + e);
-            }
+            if (p.bias || p.relu) epilogue_run<16>(p, v, col);
             if (p.c_vec && col + 16 <= p.n) {
 #pragma unroll
               for (int q = 0; q < 4; ++q)
