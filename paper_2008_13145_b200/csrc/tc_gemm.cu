@@ -451,10 +451,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* box = stage + (epi_box & 1) * (32 * 32 * 4);
           if (lane == 0) bulk_wait_read<1>();  // the store that last used this box has read it
           __syncwarp();
+          if (p.c_bf16) {
+            // bf16 box: 64-byte rows, 64B swizzle (16-byte chunk j of row r at j ^ ((r >> 1) & 3))
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
-                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4*>(box + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                             pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
@@ -740,10 +749,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* box = stage + (epi_box & 1) * (32 * 32 * 4);
           if (lane == 0) bulk_wait_read<1>();
           __syncwarp();
+          if (p.c_bf16) {
+            // bf16 box: 64-byte rows, 64B swizzle (16-byte chunk j of row r at j ^ ((r >> 1) & 3))
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
-                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4*>(box + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                             pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
@@ -950,16 +968,19 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   CUtensorMap mc;
   std::memset(&mc, 0, sizeof(mc));
   int tma_store = 0;
-  if (p.kslices <= 1 && p.c_vec && !p.c_bf16 && p.k <= kTmaStoreMaxK) {
+  // (bf16 C, KP_EPI_BF16_OUT: 32 x 32 boxes of 64-byte rows, 64B swizzle)
+  if (p.kslices <= 1 && p.c_vec && p.k <= kTmaStoreMaxK) {
+    const int ces = p.c_bf16 ? 2 : 4;
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.n), static_cast<cuuint64_t>(p.m),
                           static_cast<cuuint64_t>(p.batch)};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.ldc) * 4,
-                             static_cast<cuuint64_t>(p.batch > 1 ? p.sC : p.ldc * p.m) * 4};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.ldc) * ces,
+                             static_cast<cuuint64_t>(p.batch > 1 ? p.sC : p.ldc * p.m) * ces};
     if (p.batch == 1) strides[1] = (strides[1] + 15) / 16 * 16;
     cuuint32_t box[3] = {32, 32, 1};
     cuuint32_t es[3] = {1, 1, 1};
-    tma_store = enc(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, p.C, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+    tma_store = enc(&mc, p.c_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, p.C, dims,
+                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    p.c_bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   const bool lsu = !tma_ok(p, Cfg::ES);
