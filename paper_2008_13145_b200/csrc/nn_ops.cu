@@ -87,6 +87,45 @@ __global__ void im2col3x3_nhwc_pad_kernel(const float* __restrict__ x, int B, in
   }
 }
 
+// conv1_1 (C = 3): one thread per output pixel builds its whole padded row -- the 27
+// patch values from 9 three-float pixel reads (compile-time channel count, no integer
+// division per element), zeros up to kpad <= 32 -- and writes it as float4s (fp32 rows) or
+// 16-byte groups of 8 bf16 (round to nearest even).  Same values as the generic kernels.
+template <bool BF16>
+__global__ void im2col3x3_c3_kernel(const float* __restrict__ x, int B, int H, int W, int kpad, void* __restrict__ out,
+                                    unsigned rows) {
+  for (unsigned row = blockIdx.x * blockDim.x + threadIdx.x; row < rows; row += gridDim.x * blockDim.x) {
+    const unsigned bh = row / W;
+    const int w = static_cast<int>(row - bh * W);
+    const unsigned b = bh / H;
+    const int h = static_cast<int>(bh - b * H);
+    float v[32];
+#pragma unroll
+    for (int e = 27; e < 32; ++e) v[e] = 0.0f;
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap) {
+      const int hy = h + tap / 3 - 1, wx = w + tap % 3 - 1;
+      const bool in = hy >= 0 && hy < H && wx >= 0 && wx < W;
+      const float* src = x + ((static_cast<int64_t>(b) * H + hy) * W + wx) * 3;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[tap * 3 + c] = in ? __ldg(src + c) : 0.0f;
+    }
+    if constexpr (BF16) {
+      uint4* o = static_cast<uint4*>(out) + static_cast<int64_t>(row) * (kpad / 8);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < kpad / 8)
+          o[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                            pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+    } else {
+      float4* o = static_cast<float4*>(out) + static_cast<int64_t>(row) * (kpad / 4);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < kpad / 4) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+  }
+}
+
 // bf16 operands for the BF16 tensor-core family: im2col of fp32 NHWC activations into
 // kpad-wide bf16 rows (zeros beyond 9C), one thread per 8 columns (one 16-byte store);
 // the 8 columns are one tap's contiguous channels when C % 8 == 0 (two float4 loads),
@@ -265,6 +304,11 @@ cudaError_t im2col3x3_nhwc_pad_launch(const float* x, int B, int H, int W, int C
                                       cudaStream_t s) {
   const int64_t total4 = static_cast<int64_t>(B) * H * W * (kpad / 4);
   if (kpad % 4 != 0 || kpad < 9 * C || !aligned16(out) || total4 >= 0x7fffffffLL) return cudaErrorInvalidValue;
+  if (C == 3 && kpad <= 32) {
+    const int64_t rows = static_cast<int64_t>(B) * H * W;
+    im2col3x3_c3_kernel<false><<<grid_for(rows, 256), 256, 0, s>>>(x, B, H, W, kpad, out, static_cast<unsigned>(rows));
+    return cudaGetLastError();
+  }
   im2col3x3_nhwc_pad_kernel<<<grid_for(total4, 256), 256, 0, s>>>(x, B, H, W, C, kpad, reinterpret_cast<float4*>(out),
                                                                    static_cast<unsigned>(total4));
   return cudaGetLastError();
@@ -276,6 +320,11 @@ cudaError_t im2col3x3_nhwc_bf16_launch(const float* x, int B, int H, int W, int 
   if (kpad % 8 != 0 || kpad < 9 * C || !aligned16(out) || total8 >= 0x7fffffffLL ||
       (C % 8 == 0 && !aligned16(x)))
     return cudaErrorInvalidValue;
+  if (C == 3 && kpad <= 32) {
+    const int64_t rows = static_cast<int64_t>(B) * H * W;
+    im2col3x3_c3_kernel<true><<<grid_for(rows, 256), 256, 0, s>>>(x, B, H, W, kpad, out, static_cast<unsigned>(rows));
+    return cudaGetLastError();
+  }
   im2col3x3_nhwc_bf16_kernel<<<grid_for(total8, 256), 256, 0, s>>>(x, B, H, W, C, kpad, reinterpret_cast<uint4*>(out),
                                                                     static_cast<unsigned>(total8));
   return cudaGetLastError();
