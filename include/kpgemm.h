@@ -238,7 +238,7 @@ int kp_cast_bf16(const float* x, int64_t n, void* out, void* stream);
  * with TMA staging, i.e. CTA tile <= 256 columns, C a multiple of its k-tile depth,
  * Cout % 4 == 0; a TF32 variant with C % 32 == 0 and Cout % 4 == 0; a BF16 variant with
  * C % 64 == 0 and Cout % 8 == 0 -- the tensor-core producers load 128-byte-swizzled
- * im2col boxes into the tcgen05 ring, 1-CTA kernel), 0 when not (PAPER), < 0 for a bad
+ * im2col boxes into the tcgen05 ring, 1-CTA or CTA-pair kernel), 0 when not (PAPER), < 0 for a bad
  * id.  x, w and out must be 16-byte aligned. */
 int kp_conv3x3_supported(int id, int C, int Cout);
 int kp_conv3x3_nhwc_ex(int id, const void* x, int B, int H, int W, int C, const void* w, int Cout, void* out,

@@ -599,6 +599,15 @@ __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m
       "l"(map), "r"(bar_cluster), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
+// TMA im2col load into the pair's shared::cluster space, completion on the leader's barrier
+__device__ __forceinline__ void tma_im2col_4d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c,
+                                                   int w, int h, int n, uint16_t dx, uint16_t dy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_cluster), "r"(c), "r"(w), "r"(h), "r"(n), "h"(dx), "h"(dy)
+      : "memory");
+}
 template <bool kTF32>
 __device__ __forceinline__ void mma_issue_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                                uint32_t accum) {
@@ -692,7 +701,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* sb = sa + Cfg::A_BYTES;
         const uint32_t fbar = map_rank(&full[s], 0);
         if (leader) mbar_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
-        tma_load_3d_pair(sa, &mapA, fbar, kt * Cfg::BK, m0 + static_cast<int>(rank) * BM, za);
+        if (p.conv_c > 0) {
+          // implicit conv: this CTA's 128 pixels of the 256-row tile, one filter tap per k-tile
+          const int k0 = kt * Cfg::BK, tap = k0 / p.conv_c, c0 = k0 - tap * p.conv_c;
+          const int mr = m0 + static_cast<int>(rank) * BM;
+          const int tr = mr / p.conv_w, w = mr - tr * p.conv_w, img = tr / p.conv_h, h = tr - img * p.conv_h;
+          tma_im2col_4d_pair(sa, &mapA, fbar, c0, w - 1, h - 1, img, static_cast<uint16_t>(tap % 3),
+                             static_cast<uint16_t>(tap / 3));
+        } else {
+          tma_load_3d_pair(sa, &mapA, fbar, kt * Cfg::BK, m0 + static_cast<int>(rank) * BM, za);
+        }
 #pragma unroll
         for (int j = 0; j < Cfg::BNH / Cfg::NATOM; ++j)
           tma_load_3d_pair(sb + j * (Cfg::BK * 128), &mapB, fbar, n0 + static_cast<int>(rank) * Cfg::BNH + j * Cfg::NATOM,
@@ -777,7 +795,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (row < p.m) {
             const int col = n0 + c;
             if (p.bias || p.relu) epilogue_run<16>(p, v, col);
-            if (p.c_vec && col + 16 <= p.n) {
+            if (p.c_bf16) {
+              __nv_bfloat16* ob = static_cast<__nv_bfloat16*>(p.C) + static_cast<int64_t>(b) * p.sC +
+                                  static_cast<int64_t>(row) * p.ldc + col;
+              if (p.c_vec && col + 16 <= p.n) {
+                uint32_t w[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) w[q] = pack_bf16x2(v[2 * q], v[2 * q + 1]);
+                reinterpret_cast<uint4*>(ob)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                reinterpret_cast<uint4*>(ob)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+              } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                  if (col + e < p.n) ob[e] = __float2bfloat16_rn(v[e]);
+              }
+            } else if (p.c_vec && col + 16 <= p.n) {
 #pragma unroll
               for (int q = 0; q < 4; ++q)
                 *reinterpret_cast<float4*>(out + col + 4 * q) =
@@ -1037,7 +1069,7 @@ cudaError_t launch_tc(const GemmArgs& p0, cudaStream_t s) {
   }
   if constexpr (PAIR_STAGES > 0) {
     // CTA pairs for persistent TMA launches (no tail split: the pair kernel runs every tile)
-    if (!lsu && p.kslices <= 1 && p.conv_c == 0 && !p.c_bf16)
+    if (!lsu && p.kslices <= 1)
       return launch_pair<kTF32, BN, PAIR_STAGES>(p, ma, mb, mc, a_batched, b_batched, tma_store, s);
     tail = 0;
   }
