@@ -182,8 +182,9 @@ def conv3x3(x: torch.Tensor, w: torch.Tensor, vid: int, bias: torch.Tensor | Non
     """3x3 / stride 1 / pad 1 convolution of NHWC ``x`` (B, H, W, Cin) with the (9*Cin, Cout)
     weight matrix ``w`` (k order (dy, dx, c), as kp_im2col3x3_nhwc) as an implicit GEMM on
     SIMT, TF32 or BF16 variant ``vid`` (TMA im2col copies; kp_conv3x3_nhwc_ex).  ``x`` and
-    ``w`` are fp32 for SIMT/TF32 variants and bf16 for BF16 variants; the fp32 result,
-    (B, H, W, Cout), is bit-identical to im2col + matmul with the same variant."""
+    ``w`` are fp32 for SIMT/TF32 variants and bf16 for BF16 variants; the result,
+    (B, H, W, Cout), is bit-identical to im2col + matmul with the same variant -- fp32, or
+    rounded to bf16 when ``out`` is bf16 (tensor-core variants only, KP_EPI_BF16_OUT)."""
     dt = input_dtype(variant_info(vid)[1])
     if x.dim() != 4 or not x.is_cuda or x.dtype != dt or not x.is_contiguous():
         raise ValueError(f"x must be a contiguous (B, H, W, C) {dt} CUDA tensor for variant {vid}")
@@ -194,15 +195,16 @@ def conv3x3(x: torch.Tensor, w: torch.Tensor, vid: int, bias: torch.Tensor | Non
     cout = w.shape[1]
     if out is None:
         out = torch.empty(B, H, W, cout, device=x.device)
-    elif (out.shape != (B, H, W, cout) or out.dtype != torch.float32 or not out.is_contiguous()
-          or out.device != x.device):
-        raise ValueError(f"out must be a contiguous ({B}, {H}, {W}, {cout}) fp32 tensor on {x.device}")
+    elif (out.shape != (B, H, W, cout) or out.dtype not in (torch.float32, torch.bfloat16)
+          or not out.is_contiguous() or out.device != x.device):
+        raise ValueError(f"out must be a contiguous ({B}, {H}, {W}, {cout}) fp32 (or bf16, tensor-core "
+                         f"variants: KP_EPI_BF16_OUT) tensor on {x.device}")
+    flags = (_lib.KP_EPI_RELU if relu else 0) | (_lib.KP_EPI_BF16_OUT if out.dtype == torch.bfloat16 else 0)
     if bias is not None and (bias.shape != (cout,) or bias.dtype != torch.float32 or bias.device != x.device):
         raise ValueError(f"bias must be a ({cout},) fp32 tensor on {x.device}")
     s = (stream or torch.cuda.current_stream(x.device)).cuda_stream
     _lib.check(_lib.load().kp_conv3x3_nhwc_ex(vid, x.data_ptr(), B, H, W, C, w.data_ptr(), cout, out.data_ptr(),
-                                              bias.data_ptr() if bias is not None else None,
-                                              _lib.KP_EPI_RELU if relu else 0, s),
+                                              bias.data_ptr() if bias is not None else None, flags, s),
                f"kp_conv3x3_nhwc_ex(variant {vid}, {tuple(x.shape)} x {cout})")
     return out
 

@@ -193,6 +193,8 @@ def test_bf16_out_epilogue_equals_cast(cuda_device, family):
     assert lib.kp_conv3x3_nhwc_ex(vid, x.data_ptr(), 2, 14, 14, 64, w.data_ptr(), 128, out.data_ptr(), None,
                                   _lib.KP_EPI_RELU | _lib.KP_EPI_BF16_OUT, None) == 0
     assert torch.equal(out.view(torch.int16), ref.to(torch.bfloat16).view(torch.int16))
+    py = gemm.conv3x3(x, w, vid, relu=True, out=torch.empty_like(out))  # the Python API: bf16 out
+    assert torch.equal(py.view(torch.int16), out.view(torch.int16))
     sid = gemm.variant_id(KernelConfig(8, 8, 8, 16, 8), "simt")
     A = torch.zeros(8, 8, device=cuda_device)
     assert lib.kp_gemm_ex(sid, 8, 8, 8, 1, A.data_ptr(), 8, 0, A.data_ptr(), 8, 0, A.data_ptr(), 8, 0, None,
