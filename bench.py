@@ -27,6 +27,9 @@ batch; cpu_port = the bit-exact fmaf-chain oracle port on the same sample.
 ``--workload vgg16-infer`` is BASELINE configs[2] (images/s, data parallel);
 ``--workload sweep`` times the sharded benchmark sweep (configs[3], one LPT shard of
 problem rows per rank, no collective) and checks the merged table's canonical order.
+The default line also carries ``companions``: a short run of each of those two on the same
+ranks (so a driver ``--gpus N`` scaling run times DP inference and the sharded sweep at
+every N too); ``--no-companions`` skips them.
 """
 
 from __future__ import annotations
@@ -69,6 +72,8 @@ def parse_args(argv=None):
     ap.add_argument("--sweep-min-ms", type=float, default=1.0, help="sweep workload: timed ms per cell")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-companions", action="store_true",
+                    help="skip the short DP VGG16-inference and sharded-sweep measurements in the default line")
     return ap.parse_args(argv)
 
 
@@ -473,6 +478,33 @@ def e2e_layers(args, world, device, stream, disp, bufs, step_flops, in_dtype):
                     ", else kp_im2col3x3_nhwc" + ("_bf16" if bf16 else "") + " + Dispatcher.matmul (kp_gemm) -> D2H of every layer output"}
 
 
+# --------------------------------------------------------------- companions --
+def run_companions(args, world, rank, local):
+    """Short measurements of the other multi-GPU rows on the same ranks, so every
+    `--gpus N` run of the default line also times them at N: BASELINE configs[2] (VGG16
+    inference, data parallel by batch, 16 images per GPU, CUDA graph) and the benchmark
+    sweep sharded by LPT over the ranks (configs[3]-style, every ~10th config of the
+    family on the VGG16 problem set, 1 ms loops).  Each is its own workload's JSON line
+    (``--workload vgg16-infer`` / ``sweep``), condensed; rank 0 returns the dict."""
+    import copy
+
+    from paper_2008_13145_b200 import gemm
+
+    a = copy.copy(args)
+    a.batch, a.steps, a.warmup = 16, 10, 3
+    v = run_vgg16_infer(a, world, rank, local, emit=False)
+    s = copy.copy(args)
+    s.sweep_set, s.sweep_min_ms, s.steps, s.warmup = "vgg16", 1.0, 1, 1
+    s.sweep_stride = max(1, len(gemm.family_configs(args.family)) // 10)
+    w = run_sweep(s, world, rank, local, emit=False)
+    if rank != 0:
+        return None
+    keep = ("value", "unit", "n_gpus", "ms_per_step", "scaling", "clocks")
+    return {"vgg16_infer_dp": dict({k: v[k] for k in keep}, config=v["config"], e2e=v["e2e"], gflops=v["gflops"]),
+            "sweep_sharded": dict({k: w[k] for k in keep}, config=w["config"], shard_rows=w["shard_rows"],
+                                  merged_canonical=w["merged_canonical"])}
+
+
 # ---------------------------------------------------------------------- ours --
 def run_ours(args, world, rank, local):
     import torch
@@ -571,6 +603,8 @@ def run_ours(args, world, rank, local):
 
     e2e = None if args.no_e2e else e2e_layers(args, world, device, stream, disp, bufs, step_flops, in_dtype)
 
+    companions = None if args.no_companions else run_companions(args, world, rank, local)
+
     cpu = cpu_port = None
     if rank == 0 and world == 1 and not args.no_cpu:
         gf, secs, flops, cores = cpu_numpy_steps(args.batch, steps=1, warmup=1)
@@ -607,6 +641,8 @@ def run_ours(args, world, rank, local):
         }
         if e2e is not None:
             line["e2e"] = e2e
+        if companions is not None:
+            line["companions"] = companions
         if cpu is not None:
             line["cpu_baseline"] = cpu
             line["cpu_port"] = cpu_port
@@ -614,7 +650,7 @@ def run_ours(args, world, rank, local):
     return 0
 
 
-def run_vgg16_infer(args, world, rank, local):
+def run_vgg16_infer(args, world, rank, local, emit=True):
     """BASELINE configs[2]: VGG16 inference, fp32, tree-dispatched GEMMs, data parallel
     by batch (each rank its own images, replicated weights, no collective).  value =
     images/s over all ranks; the forward is one CUDA graph per rank."""
@@ -701,11 +737,13 @@ def run_vgg16_infer(args, world, rank, local):
                 "gpu_launches": (16 + 13 + 5) * args.steps, "clocks": clocks.summary(),
                 "e2e": {"value": args.batch * args.steps * world / (e2e_ms * 1e-3), "unit": "images/s",
                         "h2d_bytes_per_step": host_x.numel() * 4, "d2h_bytes_per_step": host_y.numel() * 4}}
+        if not emit:
+            return line
         print(json.dumps(line), flush=True)
-    return 0
+    return 0 if emit else None
 
 
-def run_sweep(args, world, rank, local):
+def run_sweep(args, world, rank, local, emit=True):
     """BASELINE configs[3]-style sweep scaling: the benchmark sweep of ``--sweep-set``
     over every ``--sweep-stride``-th config of ``--family``, problem rows sharded across
     the ranks by LPT (sweep.lpt_shards; no collective on the data path), each rank
@@ -761,7 +799,7 @@ def run_sweep(args, world, rank, local):
     ms = reduce_max(total_ms, world, device)
     barrier(world)
     if rank != 0:
-        return 0
+        return 0 if emit else None
     cells = {}
     for r in range(world):
         if shards[r]:
@@ -780,6 +818,8 @@ def run_sweep(args, world, rank, local):
             "shard_rows": [len(sh) for sh in shards], "merged_canonical": True,
             "timed_gflop_per_step": flops / 1e9, "clocks": clocks.summary(),
             "gpu_launches": None}
+    if not emit:
+        return line
     print(json.dumps(line), flush=True)
     return 0
 
