@@ -730,8 +730,10 @@ int kp_maxpool2x2_nhwc(const float* x, int B, int H, int W, int C, float* out, v
 int kp_maxpool2x2_nhwc_bf16(const void* x, int B, int H, int W, int C, void* out, void* stream) {
   if (!x || !out) return fail(KP_EINVAL, "null pointer");
   if (B < 1 || H < 2 || W < 2 || C < 1 || C % 8 != 0) return fail(KP_EINVAL, "bad activation shape (C % 8 == 0)");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(KP_EINVAL, "x and out must be 16-byte aligned");
   cudaError_t e = kp::maxpool2_nhwc_bf16_launch(x, B, H, W, C, out, static_cast<cudaStream_t>(stream));
-  return e == cudaSuccess ? KP_OK : cuda_fail(e, "maxpool (bf16) launch (x and out 16-byte aligned)");
+  return e == cudaSuccess ? KP_OK : cuda_fail(e, "maxpool (bf16) launch");
 }
 
 int kp_dispatch_load(int n_nodes, const int32_t* feature, const double* threshold, const int32_t* left,

@@ -158,6 +158,8 @@ def test_maxpool_bf16_equals_pool_then_round(cuda_device):
         assert torch.equal(out.view(torch.int16), want.contiguous().view(torch.int16))
     bad = torch.empty(1, 2, 2, 4, device=cuda_device, dtype=torch.bfloat16)
     assert lib.kp_maxpool2x2_nhwc_bf16(bad.data_ptr(), 1, 2, 2, 4, out.data_ptr(), None) == _lib.KP_EINVAL
+    x8 = torch.zeros(1, 2, 2, 16, device=cuda_device, dtype=torch.bfloat16)
+    assert lib.kp_maxpool2x2_nhwc_bf16(x8.data_ptr() + 2, 1, 2, 2, 8, out.data_ptr(), None) == _lib.KP_EINVAL
 
 
 @pytest.mark.parametrize("family", ["bf16", "tf32"])
