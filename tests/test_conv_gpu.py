@@ -201,3 +201,30 @@ def test_bf16_out_epilogue_equals_cast(cuda_device, family):
     A = torch.zeros(8, 8, device=cuda_device)
     assert lib.kp_gemm_ex(sid, 8, 8, 8, 1, A.data_ptr(), 8, 0, A.data_ptr(), 8, 0, A.data_ptr(), 8, 0, None,
                           _lib.KP_EPI_BF16_OUT, None) == _lib.KP_EINVAL
+
+
+@pytest.mark.parametrize("family,cout", [("bf16", 72), ("tf32", 68)])
+def test_tensor_core_conv_writes_stay_in_bounds(cuda_device, family, cout):
+    """Guard bands around the output (compute-sanitizer is unavailable on this pool):
+    implicit convs with ragged m (105 pixels: a partial 128-row tile, and for CTA pairs a
+    wholly out-of-range second half) and ragged Cout, fp32 and bf16 results, every config
+    of the family -- nothing is written outside the (B*H*W) x Cout output."""
+    dt = gemm.input_dtype(family)
+    B, H, W = 3, 7, 5
+    C = 64
+    g = torch.Generator(device=cuda_device).manual_seed(cout)
+    x = torch.randn(B, H, W, C, device=cuda_device, generator=g).to(dt)
+    w = (torch.randn(9 * C, cout, device=cuda_device, generator=g) * 0.05).to(dt)
+    bias = torch.randn(cout, device=cuda_device, generator=g)
+    n_out, guard = B * H * W * cout, 4096
+    lib = _lib.load()
+    for cfg in gemm.family_configs(family):
+        vid = gemm.variant_id(cfg, family)
+        for odt, flags in ((torch.float32, _lib.KP_EPI_RELU), (torch.bfloat16, _lib.KP_EPI_RELU | _lib.KP_EPI_BF16_OUT)):
+            buf = torch.full((guard + n_out + guard,), -3.0, device=cuda_device, dtype=odt)  # ReLU never writes < 0
+            out = buf[guard:guard + n_out]
+            assert lib.kp_conv3x3_nhwc_ex(vid, x.data_ptr(), B, H, W, C, w.data_ptr(), cout, out.data_ptr(),
+                                          bias.data_ptr(), flags, None) == 0
+            torch.cuda.synchronize()
+            assert bool((buf[:guard] == -3.0).all()) and bool((buf[guard + n_out:] == -3.0).all()), (cfg.as_tuple(), odt)
+            assert not bool((out == -3.0).any()), (cfg.as_tuple(), odt)  # and every element was written
