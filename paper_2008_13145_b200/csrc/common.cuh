@@ -11,6 +11,27 @@ namespace kp {
 
 // Launch parameters common to every fp32 family.  Dims follow the reference's
 // ProblemSize order (m, k, n, batch), dataset.py:61-74.
+// Division by a runtime constant d >= 1 for dividends in [0, 2^31): q = umulhi(n, mul) >> shr
+// (round-up reciprocal, mul = ceil(2^(31 + ceil(log2 d)) / d), shr = ceil(log2 d) - 1; d == 1
+// is the identity).  Host-built; replaces ~20-instruction integer divisions in the
+// single-thread TMA issue paths.
+struct FastDiv {
+  uint32_t d, mul, shr;
+  __host__ __device__ FastDiv() : d(1), mul(0), shr(0) {}
+  __host__ explicit FastDiv(uint32_t divisor) : d(divisor), mul(0), shr(0) {
+    if (divisor > 1) {
+      uint32_t lg = 0;
+      while ((1ull << lg) < divisor) ++lg;  // ceil(log2 d)
+      const uint64_t p = 31 + lg;
+      mul = static_cast<uint32_t>(((1ull << p) + divisor - 1) / divisor);
+      shr = static_cast<uint32_t>(p - 32);
+    }
+  }
+  __device__ __forceinline__ int div(int n) const {
+    return d == 1 ? n : static_cast<int>(__umulhi(static_cast<uint32_t>(n), mul) >> shr);
+  }
+};
+
 struct GemmArgs {
   int m, k, n, batch;
   const void* A;
@@ -46,6 +67,7 @@ struct GemmArgs {
   // conv_h x conv_w x conv_c) and row r / column k of the GEMM operand is the im2col
   // patch value kp_im2col3x3_nhwc would write, gathered by TMA im2col copies.
   int conv_h, conv_w, conv_c;
+  FastDiv conv_wd, conv_hd, conv_cd;  // division by conv_w, conv_h, conv_c (issue paths)
 };
 
 // Epilogue of every family: bias add (fp32, round-to-nearest) then ReLU.  Applied

@@ -390,13 +390,14 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
       f1_mbar_expect_tx(&full[stage], Cfg::T_TX_BYTES);
       if (p.conv_c > 0) {
         // implicit conv: k-tile kt lies inside one filter tap (conv_c % BK == 0)
-        const int k0 = kt * BK, tap = k0 / p.conv_c, c0 = k0 - tap * p.conv_c;
+        // (host-built reciprocals: no integer division on the issuing lane)
+        const int k0 = kt * BK, tap = p.conv_cd.div(k0), c0 = k0 - tap * p.conv_c;
         const uint16_t dy = static_cast<uint16_t>(tap / 3), dx = static_cast<uint16_t>(tap - 3 * (tap / 3));
 #pragma unroll
         for (int i = 0; i < Cfg::A_BOXES; ++i) {
           const int r = static_cast<int>(m0) + i * Cfg::A_BOX_ROWS;
-          const int t = r / p.conv_w, w = r - t * p.conv_w;
-          const int img = t / p.conv_h, h = t - img * p.conv_h;
+          const int t = p.conv_wd.div(r), w = r - t * p.conv_w;
+          const int img = p.conv_hd.div(t), h = t - img * p.conv_h;
           f1_tma_im2col_4d(as + i * Cfg::A_BOX_ROWS * SA, &maps.a, &full[stage], c0, w - 1, h - 1, img, dx, dy);
         }
       } else {
