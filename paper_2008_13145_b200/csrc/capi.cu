@@ -541,9 +541,6 @@ int kp_conv3x3_nhwc_ex(int id, const void* x, int B, int H, int W, int C, const 
   p.conv_h = H;
   p.conv_w = W;
   p.conv_c = C;
-  p.conv_hd = kp::FastDiv(static_cast<uint32_t>(H));
-  p.conv_wd = kp::FastDiv(static_cast<uint32_t>(W));
-  p.conv_cd = kp::FastDiv(static_cast<uint32_t>(C));
   return launch(id, p, static_cast<cudaStream_t>(stream));
 }
 

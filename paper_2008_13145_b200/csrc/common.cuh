@@ -13,8 +13,9 @@ namespace kp {
 // ProblemSize order (m, k, n, batch), dataset.py:61-74.
 // Division by a runtime constant d >= 1 for dividends in [0, 2^31): q = umulhi(n, mul) >> shr
 // (round-up reciprocal, mul = ceil(2^(31 + ceil(log2 d)) / d), shr = ceil(log2 d) - 1; d == 1
-// is the identity).  Host-built; replaces ~20-instruction integer divisions in the
-// single-thread TMA issue paths.
+// is the identity).  Host-built; replaces ~20-instruction integer divisions in the SIMT
+// implicit-conv issue path (carried in F1Maps, so GemmArgs -- and the GEMM instances'
+// code -- are unchanged).
 struct FastDiv {
   uint32_t d, mul, shr;
   __host__ __device__ FastDiv() : d(1), mul(0), shr(0) {}
@@ -67,7 +68,6 @@ struct GemmArgs {
   // conv_h x conv_w x conv_c) and row r / column k of the GEMM operand is the im2col
   // patch value kp_im2col3x3_nhwc would write, gathered by TMA im2col copies.
   int conv_h, conv_w, conv_c;
-  FastDiv conv_wd, conv_hd, conv_cd;  // division by conv_w, conv_h, conv_c (issue paths)
 };
 
 // Epilogue of every family: bias add (fp32, round-to-nearest) then ReLU.  Applied

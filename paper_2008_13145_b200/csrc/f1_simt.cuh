@@ -38,6 +38,7 @@ namespace kp {
 // The operand tensor maps of one launch (unused by the cp.async path).
 struct F1Maps {
   CUtensorMap a, b;
+  FastDiv cw, ch, cc;  // implicit conv: division by the image width, height and channels
 };
 
 __device__ __forceinline__ uint32_t f1_smem_u32(const void* p) {
@@ -236,10 +237,14 @@ __device__ __forceinline__ void f1_slice_reduce(const GemmArgs& p, float* smem, 
 // runs its outer products, and its lane 0 counts the stage as consumed; the warp that
 // completes the count refills the stage with the k-tile STAGES ahead.  No CTA-wide
 // barrier and no per-thread copy address math in the main loop.
-template <int R, int A, int C, int WGR, int WGC, bool TMA>
+// MODE: 0 = cp.async staging, 1 = TMA staging, 2 = TMA staging of an implicit conv (the
+// im2col issue code is compiled only into this instance, so the GEMM instances keep their
+// register allocation)
+template <int R, int A, int C, int WGR, int WGC, int MODE>
 __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCKS)
     f1_kernel(GemmArgs p, int groups_n, const __grid_constant__ F1Maps maps) {
   using Cfg = F1Cfg<R, A, C, WGR, WGC>;
+  constexpr bool TMA = MODE != 0, CONV = MODE == 2;
   constexpr int NT = Cfg::NT, BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK;
   constexpr int SA = Cfg::SA, SB = Cfg::SB, STAGES = Cfg::STAGES, VC = Cfg::VC;
   extern __shared__ __align__(16) float smem_dyn[];
@@ -388,16 +393,16 @@ __global__ void __launch_bounds__(WGR * WGC, F1Cfg<R, A, C, WGR, WGC>::MIN_BLOCK
     auto issue = [&](int stage, int kt) {  // one thread: the k-tile's boxes into a stage
       float* as = smem + stage * Cfg::T_STAGE;
       f1_mbar_expect_tx(&full[stage], Cfg::T_TX_BYTES);
-      if (p.conv_c > 0) {
+      if constexpr (CONV) {
         // implicit conv: k-tile kt lies inside one filter tap (conv_c % BK == 0)
         // (host-built reciprocals: no integer division on the issuing lane)
-        const int k0 = kt * BK, tap = p.conv_cd.div(k0), c0 = k0 - tap * p.conv_c;
+        const int k0 = kt * BK, tap = maps.cc.div(k0), c0 = k0 - tap * p.conv_c;
         const uint16_t dy = static_cast<uint16_t>(tap / 3), dx = static_cast<uint16_t>(tap - 3 * (tap / 3));
 #pragma unroll
         for (int i = 0; i < Cfg::A_BOXES; ++i) {
           const int r = static_cast<int>(m0) + i * Cfg::A_BOX_ROWS;
-          const int t = p.conv_wd.div(r), w = r - t * p.conv_w;
-          const int img = p.conv_hd.div(t), h = t - img * p.conv_h;
+          const int t = maps.cw.div(r), w = r - t * p.conv_w;
+          const int img = maps.ch.div(t), h = t - img * p.conv_h;
           f1_tma_im2col_4d(as + i * Cfg::A_BOX_ROWS * SA, &maps.a, &full[stage], c0, w - 1, h - 1, img, dx, dy);
         }
       } else {
@@ -521,8 +526,8 @@ cudaError_t f1_set_attributes() {
   using Cfg = F1Cfg<R, A, C, WGR, WGC>;
   static bool attr_set = false;  // benign race: idempotent attribute writes
   if (!attr_set) {
-    for (auto fn : {f1_kernel<R, A, C, WGR, WGC, false>, f1_kernel<R, A, C, WGR, WGC, true>}) {
-      const int bytes = fn == f1_kernel<R, A, C, WGR, WGC, true> ? Cfg::T_SMEM_BYTES : Cfg::SLICE_SMEM_BYTES;
+    for (auto fn : {f1_kernel<R, A, C, WGR, WGC, 0>, f1_kernel<R, A, C, WGR, WGC, 1>, f1_kernel<R, A, C, WGR, WGC, 2>}) {
+      const int bytes = fn == f1_kernel<R, A, C, WGR, WGC, 0> ? Cfg::SLICE_SMEM_BYTES : Cfg::T_SMEM_BYTES;
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
       if (e != cudaSuccess) return e;
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -553,8 +558,8 @@ int f1_cluster_fit(int slices) {
   for (int t = 0; t < 2; ++t) {
     int n = 0;
     lc.dynamicSmemBytes = t ? Cfg::T_SMEM_BYTES : Cfg::SLICE_SMEM_BYTES;
-    const cudaError_t e = t ? cudaOccupancyMaxActiveClusters(&n, f1_kernel<R, A, C, WGR, WGC, true>, &lc)
-                            : cudaOccupancyMaxActiveClusters(&n, f1_kernel<R, A, C, WGR, WGC, false>, &lc);
+    const cudaError_t e = t ? cudaOccupancyMaxActiveClusters(&n, f1_kernel<R, A, C, WGR, WGC, 1>, &lc)
+                            : cudaOccupancyMaxActiveClusters(&n, f1_kernel<R, A, C, WGR, WGC, 0>, &lc);
     if (e != cudaSuccess) {
       cudaGetLastError();
       return -1;
@@ -690,6 +695,11 @@ cudaError_t f1_launch(const GemmArgs& p0, cudaStream_t s) {
       have = true;
     }
     maps = last_maps;
+    if (conv) {
+      maps.cw = FastDiv(static_cast<uint32_t>(p.conv_w));
+      maps.ch = FastDiv(static_cast<uint32_t>(p.conv_h));
+      maps.cc = FastDiv(static_cast<uint32_t>(p.conv_c));
+    }
   } else {
     std::memset(&maps, 0, sizeof(maps));
   }
@@ -706,8 +716,9 @@ cudaError_t f1_launch(const GemmArgs& p0, cudaStream_t s) {
   lc.attrs = at;
   lc.numAttrs = p.kslices > 1 ? 1 : 0;
   const int gn = static_cast<int>(groups_n);
-  return tma ? cudaLaunchKernelEx(&lc, f1_kernel<R, A, C, WGR, WGC, true>, p, gn, maps)
-             : cudaLaunchKernelEx(&lc, f1_kernel<R, A, C, WGR, WGC, false>, p, gn, maps);
+  if (!tma) return cudaLaunchKernelEx(&lc, f1_kernel<R, A, C, WGR, WGC, 0>, p, gn, maps);
+  return p.conv_c > 0 ? cudaLaunchKernelEx(&lc, f1_kernel<R, A, C, WGR, WGC, 2>, p, gn, maps)
+                      : cudaLaunchKernelEx(&lc, f1_kernel<R, A, C, WGR, WGC, 1>, p, gn, maps);
 }
 
 }  // namespace kp

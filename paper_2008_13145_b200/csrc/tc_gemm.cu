@@ -96,11 +96,11 @@ __device__ __forceinline__ void tma_im2col_4d(void* dst, const CUtensorMap* map,
 struct ConvCursor {
   int w = 0, h = 0, img = 0, c0 = 0, dx = 0, dy = 0;
   __device__ __forceinline__ void start(const GemmArgs& p, int m0, int k0) {
-    const int tr = p.conv_wd.div(m0);
+    const int tr = m0 / p.conv_w;
     w = m0 - tr * p.conv_w;
-    img = p.conv_hd.div(tr);
+    img = tr / p.conv_h;
     h = tr - img * p.conv_h;
-    const int tap = p.conv_cd.div(k0);
+    const int tap = k0 / p.conv_c;
     c0 = k0 - tap * p.conv_c;
     dy = tap / 3;
     dx = tap - 3 * dy;
